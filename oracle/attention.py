@@ -1,0 +1,116 @@
+"""Attention with exact per-key EMA mass -- oracle, test infra only (float64).
+
+* ``attention``   Eq. 1: softmax(Q K^T / sqrt(d)) V, exact softmax.
+* ``chunk_attention``  the rectangular slice of Fig. 4: the m chunk
+  queries attend to all n_c cached keys plus the chunk's own keys causally
+  (reading Q10: the cache as it was *before* the chunk).  With m = 1 this is
+  Eq. 2.
+* ``rope``  rotary encoding applied by cache rank pe, rotate-half
+  pairing (i, i + d/2), inverse frequencies theta**(-2i/d), angles in float64
+  (reading Q11).
+* ``ema_weights`` / ``key_mass``  Alg. 3 in its exact-normaliser
+  reading (Q6): row r of a chunk of m queries is one EMA timestep with
+  coefficient C_EMA = (1 - gamma) * gamma**k, k = m - (r + 1), and the
+  column sum over rows of P weighted by C_EMA is the key's mass s.
+  Heads are independent per KV group and reduced with max (Q7).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def inv_freq(d: int, theta: float) -> np.ndarray:
+    return theta ** (-(np.arange(0, d, 2, dtype=np.float64)) / d)
+
+
+def rope(x: np.ndarray, pos: np.ndarray, theta: float) -> np.ndarray:
+    """Rotate rows of x[..., n, d] by positions pos[n] (rotate-half convention)."""
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    ang = np.asarray(pos, dtype=np.float64)[:, None] * inv_freq(d, theta)[None, :]
+    cos, sin = np.cos(ang), np.sin(ang)
+    x1, x2 = x[..., : d // 2], x[..., d // 2:]
+    return np.concatenate([x1 * cos - x2 * sin, x2 * cos + x1 * sin], axis=-1)
+
+
+def softmax_rows(logits: np.ndarray) -> np.ndarray:
+    mx = np.max(logits, axis=-1, keepdims=True)
+    e = np.exp(logits - mx)
+    return e / np.sum(e, axis=-1, keepdims=True)
+
+
+def attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, causal: bool,
+              scale: float | None = None) -> np.ndarray:
+    """Eq. 1 for one head: q [S, d], k [S, d], v [S, d]."""
+    d = q.shape[-1]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    logits = (q @ k.T) * scale
+    if causal:
+        S = q.shape[0]
+        logits = np.where(np.tril(np.ones((S, k.shape[0]), dtype=bool)), logits, -np.inf)
+    return softmax_rows(logits) @ v
+
+
+def chunk_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, n_cached: int,
+                    scale: float):
+    """One head of the strided-prefill slice.
+
+    q [m, d] (already rotated), k/v [n_cached + m, d] (keys rotated): rows
+    [0, n_cached) are the cache, rows n_cached + r are the chunk's own keys.
+    Query r sees every cached key and chunk keys r' <= r.  Returns (O [m, d],
+    P [m, n_cached + m]) with masked entries of P exactly 0.
+    """
+    m = q.shape[0]
+    n = k.shape[0]
+    assert n == n_cached + m
+    logits = (q @ k.T) * scale
+    r = np.arange(m)[:, None]
+    j = np.arange(n)[None, :]
+    visible = j <= n_cached + r
+    logits = np.where(visible, logits, -np.inf)
+    P = softmax_rows(logits)
+    return P @ v, P
+
+
+def ema_weights(m: int, gamma: float) -> np.ndarray:
+    """C_EMA for rows r = 0..m-1: (1 - gamma) * gamma**(m - (r + 1))."""
+    k = m - (np.arange(m) + 1)
+    return (1.0 - gamma) * np.power(gamma, k.astype(np.float64))
+
+
+def key_mass(P: np.ndarray, gamma: float) -> np.ndarray:
+    """s[j] = sum_r C_EMA[r] * P[r, j]  -- Alg. 3's column sum, exact normaliser."""
+    return ema_weights(P.shape[0], gamma) @ P
+
+
+def reduce_heads(s_heads: np.ndarray, group: int, how: str = "max") -> np.ndarray:
+    """Independent head policy: reduce each GQA group of q-heads to its kv-head.
+
+    s_heads [Hq, n] -> [Hq // group, n]."""
+    Hq, n = s_heads.shape
+    g = s_heads.reshape(Hq // group, group, n)
+    if how == "max":
+        return g.max(axis=1)
+    if how == "mean":
+        return g.mean(axis=1)
+    if how == "median":
+        return np.median(g, axis=1)
+    raise ValueError(how)
+
+
+def gamma_pow(gamma: float, m: int) -> float:
+    """gamma**m by right-to-left binary exponentiation in float64.
+
+    The decay applied to mu over a chunk of m rows (P:154 iterated m times, Q4).
+    Written out so the product order is fixed (the GPU side documents the same
+    order in include/cascade.h)."""
+    result = 1.0
+    base = float(gamma)
+    e = int(m)
+    while e > 0:
+        if e & 1:
+            result = result * base
+        base = base * base
+        e >>= 1
+    return result

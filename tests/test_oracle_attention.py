@@ -1,0 +1,241 @@
+"""Pins for oracle/attention.py and oracle/model.py against closed forms, library routines
+computed independently (torch SDPA in float64, complex-number RoPE), brute force and the
+paper's special cases."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.attention import (attention, chunk_attention, ema_weights, gamma_pow, key_mass,
+                              reduce_heads, rope)
+from oracle.model import CascadeOracle, OracleConfig
+
+
+def _rope_complex(x, pos, theta):
+    """Independent RoPE: pair (x_i, x_{i+d/2}) as a complex number times exp(i * pos * theta^(-2i/d))."""
+    d = x.shape[-1]
+    z = x[..., : d // 2] + 1j * x[..., d // 2:]
+    freqs = np.array([theta ** (-2.0 * i / d) for i in range(d // 2)])
+    z = z * np.exp(1j * np.outer(pos, freqs))
+    return np.concatenate([z.real, z.imag], axis=-1)
+
+
+def _sdpa(q, k, v, mask=None, causal=False, scale=None):
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).double()
+    out = torch.nn.functional.scaled_dot_product_attention(
+        t(q)[None], t(k)[None], t(v)[None], attn_mask=None if mask is None else torch.from_numpy(mask)[None],
+        is_causal=causal, scale=scale)
+    return out[0].numpy()
+
+
+def test_rope_matches_complex_formulation_and_is_isometry():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((37, 64))
+    pos = rng.integers(0, 70000, 37)
+    for theta in (10000.0, 500000.0):
+        a = rope(x, pos, theta)
+        # angles up to 7e4 rad: float64 angle rounding (~1e-11) dominates
+        np.testing.assert_allclose(a, _rope_complex(x, pos, theta), rtol=0, atol=5e-11)
+        np.testing.assert_allclose(np.linalg.norm(a, axis=1), np.linalg.norm(x, axis=1), rtol=1e-13)
+    np.testing.assert_array_equal(rope(x, np.zeros(37, int), 10000.0), x)     # pe 0 = identity
+
+
+def test_rope_dot_depends_on_relative_position_only():
+    rng = np.random.default_rng(1)
+    q, k = rng.standard_normal((1, 128)), rng.standard_normal((1, 128))
+    a = (rope(q, np.array([900]), 5e5) @ rope(k, np.array([100]), 5e5).T).item()
+    b = (rope(q, np.array([60800]), 5e5) @ rope(k, np.array([60000]), 5e5).T).item()
+    assert a == pytest.approx(b, rel=1e-9)
+
+
+def test_eq1_against_torch_sdpa_float64():
+    rng = np.random.default_rng(2)
+    q, k, v = (rng.standard_normal((19, 32)) for _ in range(3))
+    np.testing.assert_allclose(attention(q, k, v, causal=True), _sdpa(q, k, v, causal=True), atol=1e-13)
+    np.testing.assert_allclose(attention(q, k, v, causal=False), _sdpa(q, k, v), atol=1e-13)
+
+
+def test_spec_attention_examples():
+    # S=1 -> output = V row; one-hot limit -> V_j
+    v = np.array([[1.0, 2.0, 3.0]])
+    np.testing.assert_allclose(attention(np.ones((1, 3)), np.ones((1, 3)), v, causal=True), v)
+    K = np.eye(4)
+    V = np.arange(16.0).reshape(4, 4)
+    out = attention(200.0 * K[2:3], K, V, causal=False, scale=1.0)
+    np.testing.assert_allclose(out, V[2:3], atol=1e-12)
+
+
+def test_chunk_attention_with_empty_cache_is_causal_attention():
+    rng = np.random.default_rng(3)
+    q, k, v = (rng.standard_normal((12, 16)) for _ in range(3))
+    o, P = chunk_attention(q, k, v, 0, 0.25)
+    np.testing.assert_allclose(o, _sdpa(q, k, v, causal=True, scale=0.25), atol=1e-13)
+    np.testing.assert_allclose(P.sum(1), 1.0, atol=1e-14)
+    assert np.all(P[np.triu_indices(12, 1)] == 0.0)
+
+
+def test_chunk_attention_rectangular_slice_mask():
+    """Fig. 4: every chunk query sees the whole cache; causal among chunk keys."""
+    rng = np.random.default_rng(4)
+    n_c, m = 7, 5
+    q = rng.standard_normal((m, 8))
+    k, v = rng.standard_normal((n_c + m, 8)), rng.standard_normal((n_c + m, 8))
+    o, P = chunk_attention(q, k, v, n_c, 0.3)
+    mask = np.zeros((m, n_c + m), dtype=bool)
+    for r in range(m):
+        mask[r, : n_c + r + 1] = True
+    np.testing.assert_allclose(o, _sdpa(q, k, v, mask=mask, scale=0.3), atol=1e-13)
+    assert np.all((P > 0) == mask)
+
+
+def test_ema_weights_and_sum_rule():
+    """Alg. 3: C_EMA = beta^k (1-beta), k = len(q) - (idx+1); rows of P sum to 1, so
+    sum_j s[j] = sum_r C_EMA[r] = 1 - gamma^m (geometric series)."""
+    w = ema_weights(4, 0.5)
+    np.testing.assert_array_equal(w, [0.0625, 0.125, 0.25, 0.5])
+    rng = np.random.default_rng(5)
+    for m, n_c, gam in [(1, 5, 0.9999), (16, 30, 0.9999), (33, 0, 0.9), (64, 200, 0.99)]:
+        q = rng.standard_normal((m, 8))
+        k, v = rng.standard_normal((n_c + m, 8)), rng.standard_normal((n_c + m, 8))
+        _, P = chunk_attention(q, k, v, n_c, 0.35)
+        s = key_mass(P, gam)
+        assert s.sum() == pytest.approx(1 - gam ** m, rel=1e-12)
+        if m == 1:
+            np.testing.assert_allclose(s, (1 - gam) * P[0], rtol=1e-15)   # Eq. 2 step: s = (1-gamma) P
+
+
+def test_chunked_ema_equals_sequential_ema():
+    """SPEC criterion 4: folding a chunk of m rows (mu <- gamma^m mu + sum_r C_EMA P) equals m sequential
+    per-row EMA steps mu <- gamma mu + (1-gamma) P[r], relative 1e-9 in float64."""
+    rng = np.random.default_rng(6)
+    for _ in range(100):
+        m = int(rng.integers(1, 65))
+        n = int(rng.integers(0, 192))
+        gam = float(rng.uniform(0.5, 0.99999))
+        q = rng.standard_normal((m, 8))
+        k, v = rng.standard_normal((n + m, 8)), rng.standard_normal((n + m, 8))
+        _, P = chunk_attention(q, k, v, n, 0.4)
+        mu0 = rng.random(n + m)
+        mu0[n:] = 0.0
+        seq = mu0.copy()
+        for r in range(m):
+            seq = gam * seq + (1 - gam) * P[r]
+        chunk = gamma_pow(gam, m) * mu0 + key_mass(P, gam)
+        np.testing.assert_allclose(chunk, seq, rtol=1e-9, atol=1e-300)
+
+
+def test_gamma_pow_closed_forms():
+    assert gamma_pow(0.5, 10) == 2.0 ** -10          # exact in binary
+    assert gamma_pow(0.9999, 0) == 1.0
+    assert gamma_pow(0.0, 3) == 0.0
+    for m in (1, 7, 1024, 4096):
+        assert gamma_pow(0.9999, m) == pytest.approx(math.pow(0.9999, m), rel=4e-16 * max(1, math.log2(m) + 1))
+
+
+def test_reduce_heads_spec_example():
+    s = np.array([[0.2], [0.6]])
+    assert reduce_heads(s, 2, "mean")[0, 0] == pytest.approx(0.4)
+    assert reduce_heads(s, 2, "max")[0, 0] == 0.6
+    assert reduce_heads(s, 2, "median")[0, 0] == pytest.approx(0.4)
+    x = np.random.default_rng(0).random((8, 5))
+    r = reduce_heads(x, 4, "max")
+    assert r.shape == (2, 5) and np.all(r[0] >= x[:4]) and np.all(r[1] >= x[4:])
+
+
+def _toy_inputs(B, S, Hq, Hkv, d, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((B, S, Hq, d)), rng.standard_normal((B, S, Hkv, d)),
+            rng.standard_normal((B, S, Hkv, d)))
+
+
+@pytest.mark.parametrize("stride", [1, 7, 20, 40])
+def test_strided_prefill_below_first_drop_is_dense_rope_attention(stride):
+    """SPEC criterion 5 / P:126: with no token dropped yet (S <= alpha + 2c, Q12) every resident's
+    rank equals its stream index, so strided prefill = dense causal RoPE attention with absolute
+    positions, whatever the stride (quadratic attention is stride S)."""
+    alpha, N, c = 4, 4, 16
+    S = alpha + 2 * c            # 36: no token can have been dropped yet
+    B, Hq, Hkv, d, theta = 1, 4, 2, 16, 10000.0
+    cfg = OracleConfig(1, B, Hq, Hkv, d, alpha, N * c, N, gamma=0.99, rope_theta=theta)
+    q, k, v = _toy_inputs(B, S, Hq, Hkv, d, 11)
+    orc = CascadeOracle(cfg)
+    outs = []
+    for a in range(0, S, stride):
+        e = min(S, a + stride)
+        o, _ = orc.prefill_stride(0, q[:, a:e], k[:, a:e], v[:, a:e])
+        outs.append(o)
+    O = np.concatenate(outs, axis=1)
+    pos = np.arange(S)
+    for h in range(Hq):
+        g = h // (Hq // Hkv)
+        ref = _sdpa(_rope_complex(q[0, :, h], pos, theta), _rope_complex(k[0, :, g], pos, theta),
+                    v[0, :, g], causal=True)
+        np.testing.assert_allclose(O[0, :, h], ref, atol=1e-12)
+    st = orc.state(0)
+    assert sorted(st["origin"][0, 0][st["origin"][0, 0] >= 0]) == list(range(S))
+
+
+def test_mu_stride_invariance_below_first_drop():
+    """Chunked EMA == stride-1 EMA for every resident (1e-12 relative) while nothing is dropped.
+    One q-head per kv-head: with G > 1 the max over heads of chunk sums differs from the chunk
+    sum of per-row maxima (reading Q7 picks the former; it is unpinned for m > 1)."""
+    alpha, N, c = 4, 4, 16
+    S = alpha + 2 * c
+    B, Hq, Hkv, d = 1, 2, 2, 16
+    cfg = OracleConfig(1, B, Hq, Hkv, d, alpha, N * c, N, gamma=0.95, rope_theta=10000.0)
+    q, k, v = _toy_inputs(B, S, Hq, Hkv, d, 12)
+    mus = []
+    for stride in (1, S):
+        orc = CascadeOracle(cfg)
+        for a in range(0, S, stride):
+            orc.prefill_stride(0, q[:, a:a + stride], k[:, a:a + stride], v[:, a:a + stride])
+        st = orc.state(0)
+        order = np.argsort(st["origin"][0, 0])
+        mus.append(st["mu"][0, 0][order][st["origin"][0, 0][order] >= 0])
+    np.testing.assert_allclose(mus[0], mus[1], rtol=1e-12)
+
+
+def test_single_cascade_attention_is_sink_window_attention():
+    """N=1 = Streaming-LLM sink cache; the last chunk's attention equals masked SDPA over
+    [sinks | last |C| tokens | chunk] with rank positions."""
+    alpha, C, m, S = 3, 8, 4, 40
+    B, Hq, Hkv, d, theta = 1, 2, 1, 8, 10000.0
+    cfg = OracleConfig(1, B, Hq, Hkv, d, alpha, C, 1, gamma=0.9, rope_theta=theta)
+    q, k, v = _toy_inputs(B, S, Hq, Hkv, d, 13)
+    orc = CascadeOracle(cfg)
+    for a in range(0, S - m, m):
+        orc.prefill_stride(0, q[:, a:a + m], k[:, a:a + m], v[:, a:a + m])
+    a = S - m
+    O, _ = orc.prefill_stride(0, q[:, a:], k[:, a:], v[:, a:])
+    keep = list(range(alpha)) + list(range(a - C, a)) + list(range(a, S))
+    n_c = alpha + C
+    pos = np.arange(len(keep))
+    mask = np.zeros((m, len(keep)), dtype=bool)
+    for r in range(m):
+        mask[r, : n_c + r + 1] = True
+    for h in range(Hq):
+        ref = _sdpa(_rope_complex(q[0, a:, h], n_c + np.arange(m), theta),
+                    _rope_complex(k[0, keep, 0], pos, theta), v[0, keep, 0], mask=mask)
+        np.testing.assert_allclose(O[0, :, h], ref, atol=1e-12)
+
+
+def test_decode_is_prefill_with_stride_one_and_eq2():
+    """Eq. 2: one token attends to C_K U new key; s = (1-gamma) * P."""
+    alpha, N, c = 2, 2, 3
+    B, Hq, Hkv, d = 1, 2, 1, 8
+    cfg = OracleConfig(1, B, Hq, Hkv, d, alpha, N * c, N, gamma=0.9, rope_theta=10000.0)
+    q, k, v = _toy_inputs(B, 6, Hq, Hkv, d, 14)
+    orc = CascadeOracle(cfg)
+    orc.prefill_stride(0, q[:, :5], k[:, :5], v[:, :5])
+    O, s = orc.decode(0, q[:, 5], k[:, 5], v[:, 5])
+    pos = np.arange(6)
+    logits = np.array([_rope_complex(q[0, 5:6, h], [5], 10000.0) @ _rope_complex(k[0, :, 0], pos, 10000.0).T
+                       for h in range(Hq)])[:, 0] / math.sqrt(d)
+    P = np.exp(logits - logits.max(1, keepdims=True))
+    P /= P.sum(1, keepdims=True)
+    np.testing.assert_allclose(O[0], P @ v[0, :, 0], atol=1e-13)
+    # all 6 tokens resident (5 + new): s over [cache(5) | new] equals (1-gamma) max_h P
+    s_flat = s[0, 0]
+    np.testing.assert_allclose(np.sort(s_flat[s_flat > 0]), np.sort(0.1 * P.max(0)), rtol=1e-13)
