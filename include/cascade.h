@@ -1,0 +1,201 @@
+/*
+ * cascade.h -- C ABI of the B200 (sm_100a) Cascading KV Cache hot path.
+ *
+ * Method: arXiv 2406.17808, "Training-Free Exact Extension of Context Length
+ * for LLMs via Cascading KV Cache".  Citations "P:n" are lines of the paper's
+ * LaTeX; "Qn" are the readings listed in DESIGN.md.
+ *
+ * One handle holds, for every (layer l, sequence b, kv-head g), the cascade of
+ * PAPER.md section 3.1: a sink buffer of alpha tokens plus N
+ * sub-caches of c = |C|/N slots kept as circular buffers with an oldest-slot
+ * pointer xi, the EMA score mu of every cached token
+ * and its stream index ("origin").  Calls are:
+ *
+ *   cascade_prefill_stride  one step of Alg. 1 for one layer: the
+ *                           m chunk queries attend to [sinks | cached slots |
+ *                           chunk keys (causal)] (Fig. 4), the
+ *                           per-key EMA mass of Alg. 3 (exact
+ *                           normaliser, Q6) is reduced with max over each GQA
+ *                           group, folded into mu (Q4) and the m
+ *                           tokens are inserted with Alg. 2.
+ *   cascade_decode          the m = 1 case (Eq. 2).
+ *   cascade_state           export of the cascade state of a layer.
+ *
+ * Conventions shared with the oracle:
+ *   flat slot of sink s          = s                       (0 <= s < alpha)
+ *   flat slot of ring slot s of
+ *   sub-cache i (1-indexed)      = alpha + (i-1)*c + s     (0 <= s < c)
+ *   chunk row r (scores only)    = S_tot + r,  S_tot = alpha + |C|
+ *   Sub-cache i accepts the token with 0-based stream index t iff
+ *   t mod 2^(i-1) == 0, t counting sink insertions too (reading Q1).
+ *   Selection keeps the resident on ties (strict '>').
+ *   pe of a resident = its rank in [sinks; C_N oldest..newest; ...; C_1]
+ *   (P:158); chunk token r gets pe = n_cached + r.  Keys are cached
+ *   pre-RoPE; RoPE is rotate-half with inv_freq_i = theta^(-2i/d).
+ *   The decay per chunk is g = gamma^m computed on the host in double by
+ *   right-to-left binary exponentiation (result *= base when the bit is set,
+ *   then base *= base); the fold is mu <- g*mu + s in IEEE double with no
+ *   fused multiply-add; a new token starts at mu = s.
+ *
+ * Memory: the caller owns every device buffer.  The library never calls
+ * cudaMalloc; it carves the caller's workspace (cascade_workspace_bytes) and
+ * allocates only a small pinned host ring for schedule uploads.  All device
+ * pointers must be on `device`, contiguous, 16-byte aligned.
+ *
+ * Ordering: calls on one layer must be issued in order on one stream (the
+ * handle keeps a host mirror of the cascade counters so no call needs a
+ * device->host synchronisation).  Different layers may use different streams.
+ * A handle is single-writer: do not call into one handle from two threads.
+ *
+ * Errors: every entry point validates on the host before launching anything;
+ * on a non-OK return no device state changed and the mirror did not advance.
+ * CASCADE_ERR_CUDA reports a launch/copy error (cudaGetLastError); device
+ * faults surface at the next synchronisation, as CUDA does.
+ */
+#ifndef CASCADE_H_
+#define CASCADE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CASCADE_MAX_LEVELS 16
+
+typedef enum {
+  CASCADE_OK = 0,
+  CASCADE_ERR_INVALID_ARG = -1, /* null pointer, bad layer index, ...           */
+  CASCADE_ERR_CONFIG = -2,      /* |C| % N != 0, gamma not in [0,1], Hq % Hkv, d */
+  CASCADE_ERR_SHAPE = -3,       /* m < 1 or m > max_stride                       */
+  CASCADE_ERR_ORDER = -4,       /* reserved: call out of order                   */
+  CASCADE_ERR_WORKSPACE = -5,   /* workspace too small or misaligned             */
+  CASCADE_ERR_CUDA = -6,        /* CUDA launch / copy error                      */
+  CASCADE_ERR_UNSUPPORTED = -7  /* option not implemented in this build         */
+} cascade_status;
+
+typedef enum { CASCADE_F32 = 0, CASCADE_BF16 = 1 } cascade_dtype;
+
+typedef struct {
+  int32_t num_layers;    /* L >= 1                                              */
+  int32_t batch;         /* B >= 1 independent sequences                */
+  int32_t num_q_heads;   /* Hq                                                  */
+  int32_t num_kv_heads;  /* Hkv, Hq % Hkv == 0 (GQA)                 */
+  int32_t head_dim;      /* d in {64, 128}                                      */
+  int32_t sink_size;     /* alpha >= 0 (64 in the paper)          */
+  int32_t cache_size;    /* |C| >= N, excludes the sinks (Q16)           */
+  int32_t num_cascades;  /* N in [1, CASCADE_MAX_LEVELS], |C| % N == 0 (Q14)    */
+  int32_t max_stride;    /* largest m a call may pass (sizes scratch)           */
+  int32_t dtype;         /* cascade_dtype of q/k/v/out and the cached K/V       */
+  double ema_gamma;      /* gamma in [0,1] (0.9999 in the paper)  */
+  double rope_theta;     /* RoPE base > 0 (Q11)                                 */
+  double softmax_scale;  /* 0 -> 1/sqrt(d) (Eq. 1)                              */
+  int32_t head_policy;   /* 0 = independent heads; others unsupported   */
+  int32_t head_reduce;   /* 0 = max over the GQA group; others unsupp.  */
+  int32_t selection;     /* 1 = EMA token selection; 0 unsupported      */
+  int32_t reserved;
+} cascade_config;
+
+/* Host mirror of one layer's cascade counters (identical for all b, g). */
+typedef struct {
+  int64_t t;                               /* tokens offered so far            */
+  int32_t sink_count;                      /* residents of the sink buffer     */
+  int32_t counts[CASCADE_MAX_LEVELS];      /* residents of sub-cache i+1       */
+  int32_t xi[CASCADE_MAX_LEVELS];          /* oldest slot of sub-cache i+1     */
+} cascade_mirror;
+
+typedef struct {
+  cascade_mirror mirror;
+  int32_t num_cascades, sub_cache_size, sink_size, slots_total; /* N, c, alpha, S_tot */
+  int32_t head_dim, dtype, batch, num_kv_heads;
+  int32_t n_cached;                        /* sink_count + sum(counts)          */
+  /* Device pointers, layout [B][Hkv][S_tot](+[d]) for this layer:            */
+  void* k_raw;        /* pre-RoPE keys, dtype                                  */
+  void* v;            /* values, dtype                                         */
+  double* mu;         /* EMA score, 0 for empty slots                          */
+  int64_t* origin;    /* stream index, -1 for empty slots                      */
+  int32_t* pe;        /* [S_tot] rank position, -1 for empty (head-independent)*/
+} cascade_state_view;
+
+typedef struct cascade_handle cascade_handle;
+
+const char* cascade_status_string(cascade_status s);
+
+/* Validates cfg (host only).  Returns CASCADE_OK or the error it would raise. */
+cascade_status cascade_validate_config(const cascade_config* cfg);
+
+/* Device bytes the caller must provide to cascade_init (0 if cfg is invalid). */
+size_t cascade_workspace_bytes(const cascade_config* cfg);
+
+/* Carves d_ws (ws_bytes >= cascade_workspace_bytes, 256-B aligned) and
+ * initialises every cascade to empty: origin = -1, mu = 0, counters 0.  Uses
+ * cudaMemsetAsync + one synchronisation (init is off the hot path).  *out is
+ * a host object owned by the library; free it with cascade_destroy. */
+cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_bytes,
+                            int device, cascade_handle** out);
+
+void cascade_destroy(cascade_handle* h);
+
+/* One Alg. 1 step for one layer, all B sequences and heads.
+ *   q   [B, m, Hq,  d] device, dtype   chunk queries (pre-RoPE)
+ *   k   [B, m, Hkv, d] device, dtype   chunk keys (pre-RoPE; cached raw)
+ *   v   [B, m, Hkv, d] device, dtype
+ *   out [B, m, Hq,  d] device, dtype   attention output (written)
+ *   stream: a cudaStream_t (NULL = legacy default stream).
+ * Advances the layer's t by m.  Inputs are read-only and may be reused by the
+ * caller as soon as the stream reaches the end of this call. */
+cascade_status cascade_prefill_stride(cascade_handle* h, int32_t layer, const void* q,
+                                      const void* k, const void* v, int32_t m, void* out,
+                                      void* stream);
+
+/* Same as cascade_prefill_stride but q/k/v/out are HOST buffers (pinned for
+ * asynchronous copies).  The host->device and device->host copies run on
+ * `stream` through a staging area inside the workspace; the call returns after
+ * `out` is written (it synchronises the stream).  Calls of this variant must
+ * not run concurrently on two streams of one handle. */
+cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, const void* q,
+                                           const void* k, const void* v, int32_t m, void* out,
+                                           void* stream);
+
+/* Single-token step (Eq. 2) + update, m = 1.
+ *   q [B, Hq, d], k/v [B, Hkv, d], out [B, Hq, d], device, dtype. */
+cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,
+                              const void* v, void* out, void* stream);
+
+/* Synchronises `stream`, writes the pe array of the layer on the device and
+ * fills *out (host struct with device pointers into the workspace). */
+cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out,
+                             void* stream);
+
+/* ---- test hooks -------------------------------------------------------- */
+
+/* Score injection: fold the given per-key mass and insert the m tokens, with
+ * no attention.  s [B, Hkv, S_tot + m] fp32 device, flat slot space (chunk
+ * row r at S_tot + r; entries of empty slots are ignored).  k/v as in
+ * cascade_prefill_stride.  Used for bit-exact state parity. */
+cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, const void* k,
+                                          const void* v, int32_t m, const float* s, void* stream);
+
+/* Copies the per-key mass s of the layer's last prefill/decode into
+ * out [B, Hkv, S_tot + m_last] fp32 device (flat slot space, 0 for empty slots).
+ * *m_last receives that call's m. */
+cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out, int32_t* m_last,
+                                   void* stream);
+
+/* Host-only (no device needed): advance a mirror by m insertions exactly as
+ * the library does and optionally write the pe of every flat slot after the
+ * advance (pe_out [S_tot], -1 for empty) and operation counts
+ * (ops_out[4] = {selects, final slot writes, drops, select dependency depth}). */
+cascade_status cascade_mirror_advance(const cascade_config* cfg, cascade_mirror* mirror,
+                                      int32_t m, int32_t* pe_out, int64_t* ops_out);
+
+/* Number of kernel launches issued by this handle since init (for the bench's
+ * gpu_launches count). */
+int64_t cascade_launch_count(const cascade_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CASCADE_H_ */

@@ -34,6 +34,17 @@ def rope(x: np.ndarray, pos: np.ndarray, theta: float) -> np.ndarray:
     return np.concatenate([x1 * cos - x2 * sin, x2 * cos + x1 * sin], axis=-1)
 
 
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bfloat16 (ties to even), via float32 -- returned as float64.
+
+    bfloat16 is the top 16 bits of an IEEE float32; rounding adds 0x7fff plus the lowest
+    kept bit before truncating the low 16 bits (round-to-nearest-even)."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
 def softmax_rows(logits: np.ndarray) -> np.ndarray:
     mx = np.max(logits, axis=-1, keepdims=True)
     e = np.exp(logits - mx)

@@ -26,7 +26,7 @@ from typing import Dict, List
 
 import numpy as np
 
-from .attention import chunk_attention, gamma_pow, key_mass, reduce_heads, rope
+from .attention import chunk_attention, gamma_pow, key_mass, reduce_heads, rope, round_bf16
 from .cascade import CascadeHead, Token
 
 
@@ -44,6 +44,10 @@ class OracleConfig:
     rope_theta: float = 10000.0
     softmax_scale: float = 0.0        # 0 -> 1/sqrt(d)
     selection: bool = True
+    # Reading Q17: in the bf16 configs the rotated q and k are the operands the score
+    # products consume, held in bf16 (the model dtype the paper's kernel runs in); the
+    # oracle rounds them to bf16 (round-to-nearest-even) before its float64 dot products.
+    round_operands: str = ""          # "" or "bf16"
 
     @property
     def c(self) -> int:
@@ -121,10 +125,14 @@ class CascadeOracle:
                 v_all = np.concatenate([np.array(vc).reshape(n_c, d),
                                         np.asarray(v[b, :, g], np.float64)], axis=0)
                 k_rot = rope(k_all, np.arange(n_c + m), cfg.rope_theta)
+                if cfg.round_operands == "bf16":
+                    k_rot = round_bf16(k_rot)
                 s_h = np.zeros((G, n_c + m))
                 for j in range(G):
                     h = g * G + j
                     q_rot = rope(np.asarray(q[b, :, h], np.float64), n_c + np.arange(m), cfg.rope_theta)
+                    if cfg.round_operands == "bf16":
+                        q_rot = round_bf16(q_rot)
                     o_h, P = chunk_attention(q_rot, k_rot, v_all, n_c, cfg.scale)
                     O[b, :, h] = o_h
                     s_h[j] = key_mass(P, cfg.gamma)

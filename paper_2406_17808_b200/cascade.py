@@ -1,0 +1,286 @@
+"""Thin ctypes binding of libcascade.so (include/cascade.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; PyTorch only provides
+device memory (the workspace and I/O tensors) and streams.  There is no CPU fallback:
+if the shared library is missing this module raises on import of the library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcascade.so")
+
+MAX_LEVELS = 16
+F32, BF16 = 0, 1
+_STATUS = {0: "ok", -1: "invalid argument", -2: "invalid config", -3: "bad shape",
+           -4: "call out of order", -5: "workspace", -6: "CUDA error", -7: "unsupported"}
+
+
+class CascadeError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {_STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("sink_size", ctypes.c_int32),
+                ("cache_size", ctypes.c_int32), ("num_cascades", ctypes.c_int32),
+                ("max_stride", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("ema_gamma", ctypes.c_double), ("rope_theta", ctypes.c_double),
+                ("softmax_scale", ctypes.c_double), ("head_policy", ctypes.c_int32),
+                ("head_reduce", ctypes.c_int32), ("selection", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class Mirror(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("sink_count", ctypes.c_int32),
+                ("counts", ctypes.c_int32 * MAX_LEVELS), ("xi", ctypes.c_int32 * MAX_LEVELS)]
+
+
+class _StateView(ctypes.Structure):
+    _fields_ = [("mirror", Mirror), ("num_cascades", ctypes.c_int32),
+                ("sub_cache_size", ctypes.c_int32), ("sink_size", ctypes.c_int32),
+                ("slots_total", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("n_cached", ctypes.c_int32),
+                ("k_raw", ctypes.c_void_p), ("v", ctypes.c_void_p), ("mu", ctypes.c_void_p),
+                ("origin", ctypes.c_void_p), ("pe", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libcascade.so once; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2406_17808_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, cfgp = ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(_Config)
+        sig = {
+            "cascade_status_string": (ctypes.c_char_p, [i32]),
+            "cascade_validate_config": (i32, [cfgp]),
+            "cascade_workspace_bytes": (ctypes.c_size_t, [cfgp]),
+            "cascade_init": (i32, [cfgp, vp, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(vp)]),
+            "cascade_destroy": (None, [vp]),
+            "cascade_prefill_stride": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
+            "cascade_prefill_stride_host": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
+            "cascade_decode": (i32, [vp, i32, vp, vp, vp, vp, vp]),
+            "cascade_state": (i32, [vp, i32, ctypes.POINTER(_StateView), vp]),
+            "cascade_update_with_scores": (i32, [vp, i32, vp, vp, i32, vp, vp]),
+            "cascade_last_scores": (i32, [vp, i32, vp, ctypes.POINTER(i32), vp]),
+            "cascade_mirror_advance": (i32, [cfgp, ctypes.POINTER(Mirror), i32, vp, vp]),
+            "cascade_launch_count": (ctypes.c_int64, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["cascade_status_string", "cascade_validate_config", "cascade_workspace_bytes",
+            "cascade_init", "cascade_destroy", "cascade_prefill_stride",
+            "cascade_prefill_stride_host", "cascade_decode", "cascade_state",
+            "cascade_update_with_scores", "cascade_last_scores", "cascade_mirror_advance",
+            "cascade_launch_count"]
+
+
+@dataclass
+class CascadeConfig:
+    num_layers: int = 1
+    batch: int = 1
+    num_q_heads: int = 32
+    num_kv_heads: int = 8
+    head_dim: int = 128
+    sink_size: int = 64
+    cache_size: int = 4096
+    num_cascades: int = 4
+    max_stride: int = 1024
+    dtype: str = "bf16"
+    ema_gamma: float = 0.9999
+    rope_theta: float = 500000.0
+    softmax_scale: float = 0.0
+
+    def c_struct(self) -> _Config:
+        return _Config(self.num_layers, self.batch, self.num_q_heads, self.num_kv_heads,
+                       self.head_dim, self.sink_size, self.cache_size, self.num_cascades,
+                       self.max_stride, BF16 if self.dtype == "bf16" else F32,
+                       self.ema_gamma, self.rope_theta, self.softmax_scale, 0, 0, 1, 0)
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.dtype == "bf16" else torch.float32
+
+    @property
+    def c(self) -> int:
+        return self.cache_size // self.num_cascades
+
+    @property
+    def s_tot(self) -> int:
+        return self.sink_size + self.cache_size
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != 0:
+        raise CascadeError(rc, where)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class _DevArray:
+    """Exposes a device pointer to torch through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 2, "strides": None}
+
+
+def workspace_bytes(cfg: CascadeConfig) -> int:
+    return int(lib().cascade_workspace_bytes(ctypes.byref(cfg.c_struct())))
+
+
+def validate(cfg: CascadeConfig) -> int:
+    return int(lib().cascade_validate_config(ctypes.byref(cfg.c_struct())))
+
+
+def mirror_advance(cfg: CascadeConfig, mirror: Mirror, m: int, want_pe=True, want_ops=True):
+    """Host-only mirror advance (no GPU): returns (pe [S_tot] list or None, ops [4] list or None)."""
+    import numpy as np
+    pe = np.zeros(cfg.s_tot, dtype=np.int32) if want_pe else None
+    ops = np.zeros(4, dtype=np.int64) if want_ops else None
+    rc = lib().cascade_mirror_advance(ctypes.byref(cfg.c_struct()), ctypes.byref(mirror), m,
+                                      None if pe is None else pe.ctypes.data_as(ctypes.c_void_p),
+                                      None if ops is None else ops.ctypes.data_as(ctypes.c_void_p))
+    _check(rc, "cascade_mirror_advance")
+    return pe, ops
+
+
+class Cascade:
+    """One library handle: the cascades of every (layer, sequence, kv-head) on one device."""
+
+    def __init__(self, cfg: CascadeConfig, device: int = 0):
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        L = lib()
+        cs = cfg.c_struct()
+        rc = L.cascade_validate_config(ctypes.byref(cs))
+        _check(rc, "cascade_validate_config")
+        nbytes = int(L.cascade_workspace_bytes(ctypes.byref(cs)))
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        off = (-base) % 256
+        self._h = ctypes.c_void_p()
+        rc = L.cascade_init(ctypes.byref(cs), ctypes.c_void_p(base + off), nbytes, device,
+                            ctypes.byref(self._h))
+        _check(rc, "cascade_init")
+
+    def close(self):
+        if self._h:
+            lib().cascade_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- hot path ------------------------------------------------------------
+    def prefill_stride(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                       out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        B, m, Hq, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        for t in (q, k, v, out):
+            assert t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        rc = lib().cascade_prefill_stride(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m, _ptr(out),
+                                          _stream(stream))
+        _check(rc, "cascade_prefill_stride")
+        return out
+
+    def prefill_stride_host(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                            out: torch.Tensor, stream=None) -> torch.Tensor:
+        """q/k/v/out are (pinned) host tensors; copies happen inside the library call."""
+        m = q.shape[1]
+        for t in (q, k, v, out):
+            assert not t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        rc = lib().cascade_prefill_stride_host(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m,
+                                               _ptr(out), _stream(stream))
+        _check(rc, "cascade_prefill_stride_host")
+        return out
+
+    def decode(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+               out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty_like(q)
+        for t in (q, k, v, out):
+            assert t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        rc = lib().cascade_decode(self._h, layer, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _stream(stream))
+        _check(rc, "cascade_decode")
+        return out
+
+    # ---- test hooks / export ---------------------------------------------------
+    def update_with_scores(self, layer: int, k: torch.Tensor, v: torch.Tensor, s: torch.Tensor,
+                           stream=None) -> None:
+        m = k.shape[1]
+        assert s.dtype == torch.float32 and s.is_cuda and s.is_contiguous()
+        assert s.shape == (self.cfg.batch, self.cfg.num_kv_heads, self.cfg.s_tot + m)
+        rc = lib().cascade_update_with_scores(self._h, layer, _ptr(k), _ptr(v), m, _ptr(s),
+                                              _stream(stream))
+        _check(rc, "cascade_update_with_scores")
+
+    def last_scores(self, layer: int, stream=None) -> torch.Tensor:
+        m = ctypes.c_int32(0)
+        # query m first with a dummy call that fails on size? -> keep a max-size buffer
+        out = torch.empty((self.cfg.batch, self.cfg.num_kv_heads, self.cfg.s_tot + self.cfg.max_stride),
+                          dtype=torch.float32, device=self.device)
+        rc = lib().cascade_last_scores(self._h, layer, _ptr(out), ctypes.byref(m), _stream(stream))
+        _check(rc, "cascade_last_scores")
+        n = self.cfg.s_tot + m.value
+        flat = out.view(-1)[: self.cfg.batch * self.cfg.num_kv_heads * n]
+        return flat.view(self.cfg.batch, self.cfg.num_kv_heads, n).clone()
+
+    def state(self, layer: int, stream=None) -> dict:
+        """Copies of the layer's cascade state (torch tensors on the device) + the mirror."""
+        sv = _StateView()
+        rc = lib().cascade_state(self._h, layer, ctypes.byref(sv), _stream(stream))
+        _check(rc, "cascade_state")
+        B, Hk, S, d = self.cfg.batch, self.cfg.num_kv_heads, sv.slots_total, self.cfg.head_dim
+        ts = "<f4" if self.cfg.dtype == "f32" else "<i2"
+
+        def dev(ptr, shape, typestr, dtype=None):
+            t = torch.as_tensor(_DevArray(ptr, shape, typestr), device=self.device).clone()
+            return t.view(dtype) if dtype is not None else t
+
+        kdt = torch.float32 if self.cfg.dtype == "f32" else torch.bfloat16
+        mr = sv.mirror
+        N = sv.num_cascades
+        return dict(
+            t=int(mr.t), sink_count=int(mr.sink_count), counts=[int(x) for x in mr.counts[:N]],
+            xi=[int(x) for x in mr.xi[:N]], n_cached=int(sv.n_cached),
+            k=dev(sv.k_raw, (B, Hk, S, d), ts, kdt), v=dev(sv.v, (B, Hk, S, d), ts, kdt),
+            mu=dev(sv.mu, (B, Hk, S), "<f8"), origin=dev(sv.origin, (B, Hk, S), "<i8"),
+            pe=dev(sv.pe, (S,), "<i4"))
+
+    def launch_count(self) -> int:
+        return int(lib().cascade_launch_count(self._h))

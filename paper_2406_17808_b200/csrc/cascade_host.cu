@@ -1,0 +1,451 @@
+// cascade_host.cu -- the C ABI (include/cascade.h): validation, workspace carve, host
+// mirror, schedule upload and the launch sequence of each call.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+#include "plan.h"
+
+using namespace cascade;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kRing = 8;   // pinned schedule staging buffers in flight
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+size_t elem_size(int32_t dtype) { return dtype == CASCADE_BF16 ? 2 : 4; }
+
+struct LayerBufs {
+  // persistent state
+  void* k_raw; void* v; double* mu; int64_t* origin; int32_t* pe;
+  // per-call scratch (per layer so layers may run on different streams)
+  float* s; float* lse; int32_t* plan; int32_t* resolved;
+  void* q_rot; void* k_rot; void* v_chunk;
+};
+
+struct Sizes {
+  size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
+  size_t per_layer;
+  size_t rope_tab, stage_q, stage_kv, stage_out;
+  size_t total;
+  int32_t plan_ints;
+};
+
+Sizes compute_sizes(const cascade_config& c) {
+  Sizes z{};
+  const size_t es = elem_size(c.dtype);
+  const size_t B = c.batch, Hq = c.num_q_heads, Hk = c.num_kv_heads, d = c.head_dim;
+  const size_t S = (size_t)c.sink_size + c.cache_size, M = c.max_stride;
+  const size_t N = c.num_cascades;
+  z.k_raw = align_up(B * Hk * S * d * es);
+  z.v = z.k_raw;
+  z.mu = align_up(B * Hk * S * 8);
+  z.origin = z.mu;
+  z.pe = align_up(S * 4);
+  z.s = align_up(B * Hk * (S + M) * 4);
+  z.lse = align_up(B * Hq * M * 4);
+  // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats)
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + M + 16);
+  z.plan = align_up((size_t)z.plan_ints * 4);
+  z.resolved = align_up(B * Hk * M * 4);
+  z.q_rot = align_up(B * Hq * M * d * es);
+  z.k_rot = align_up(B * Hk * (S + M) * d * es);
+  z.v_chunk = align_up(B * Hk * M * d * es);
+  z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
+                z.q_rot + z.k_rot + z.v_chunk;
+  z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
+  z.stage_q = align_up(B * M * Hq * d * es);
+  z.stage_kv = align_up(B * M * Hk * d * es);
+  z.stage_out = z.stage_q;
+  z.total = z.per_layer * c.num_layers + z.rope_tab + z.stage_q + 2 * z.stage_kv + z.stage_out;
+  return z;
+}
+
+}  // namespace
+
+struct cascade_handle {
+  cascade_config cfg;
+  int device;
+  Sizes sz;
+  int32_t alpha, N, c, S_tot;
+  std::vector<LayerBufs> layers;
+  std::vector<cascade_mirror> mirrors;
+  std::vector<int32_t> m_last;
+  float2* rope_tab;
+  void *stage_q, *stage_k, *stage_v, *stage_out;
+  Planner planner;
+  Plan plan;
+  int32_t* pinned[kRing];
+  cudaEvent_t ring_ev[kRing];
+  int ring_pos;
+  int64_t launches;
+};
+
+extern "C" {
+
+const char* cascade_status_string(cascade_status s) {
+  switch (s) {
+    case CASCADE_OK: return "ok";
+    case CASCADE_ERR_INVALID_ARG: return "invalid argument";
+    case CASCADE_ERR_CONFIG: return "invalid config";
+    case CASCADE_ERR_SHAPE: return "bad shape (m < 1 or m > max_stride)";
+    case CASCADE_ERR_ORDER: return "call out of order";
+    case CASCADE_ERR_WORKSPACE: return "workspace too small or misaligned";
+    case CASCADE_ERR_CUDA: return "CUDA error";
+    case CASCADE_ERR_UNSUPPORTED: return "unsupported option";
+  }
+  return "unknown status";
+}
+
+cascade_status cascade_validate_config(const cascade_config* c) {
+  if (!c) return CASCADE_ERR_INVALID_ARG;
+  if (c->num_layers < 1 || c->batch < 1 || c->num_q_heads < 1 || c->num_kv_heads < 1)
+    return CASCADE_ERR_CONFIG;
+  if (c->num_q_heads % c->num_kv_heads) return CASCADE_ERR_CONFIG;
+  if (c->head_dim != 64 && c->head_dim != 128) return CASCADE_ERR_CONFIG;
+  if (c->sink_size < 0 || c->num_cascades < 1 || c->num_cascades > CASCADE_MAX_LEVELS)
+    return CASCADE_ERR_CONFIG;
+  if (c->cache_size < c->num_cascades || c->cache_size % c->num_cascades) return CASCADE_ERR_CONFIG;
+  if (!(c->ema_gamma >= 0.0 && c->ema_gamma <= 1.0)) return CASCADE_ERR_CONFIG;
+  if (!(c->rope_theta > 0.0) || c->softmax_scale < 0.0) return CASCADE_ERR_CONFIG;
+  if (c->max_stride < 1) return CASCADE_ERR_CONFIG;
+  if (c->dtype != CASCADE_F32 && c->dtype != CASCADE_BF16) return CASCADE_ERR_CONFIG;
+  if (c->head_policy != 0 || c->head_reduce != 0 || c->selection != 1) return CASCADE_ERR_UNSUPPORTED;
+  const long long S = (long long)c->sink_size + c->cache_size;
+  if (S + c->max_stride > (1LL << 30)) return CASCADE_ERR_CONFIG;
+  return CASCADE_OK;
+}
+
+size_t cascade_workspace_bytes(const cascade_config* c) {
+  if (cascade_validate_config(c) != CASCADE_OK) return 0;
+  return compute_sizes(*c).total;
+}
+
+cascade_status cascade_mirror_advance(const cascade_config* cfg, cascade_mirror* mirror, int32_t m,
+                                      int32_t* pe_out, int64_t* ops_out) {
+  cascade_status st = cascade_validate_config(cfg);
+  if (st != CASCADE_OK) return st;
+  if (!mirror) return CASCADE_ERR_INVALID_ARG;
+  if (m < 0) return CASCADE_ERR_SHAPE;
+  const int32_t N = cfg->num_cascades, c = cfg->cache_size / N;
+  Planner p;
+  p.configure(cfg->sink_size, N, c);
+  Plan plan;
+  p.advance(*mirror, m, ops_out ? &plan : nullptr);
+  if (pe_out) mirror_positions(*mirror, cfg->sink_size, N, c, pe_out);
+  if (ops_out) {
+    ops_out[0] = (int64_t)plan.sel_depth.size();
+    ops_out[1] = (int64_t)plan.mov.size() / 2;
+    ops_out[2] = plan.drops;
+    ops_out[3] = (int64_t)plan.depth_begin.size() - 1;
+  }
+  return CASCADE_OK;
+}
+
+void cascade_destroy(cascade_handle* h) {
+  if (!h) return;
+  for (int i = 0; i < kRing; ++i) {
+    if (h->ring_ev[i]) cudaEventDestroy(h->ring_ev[i]);
+    if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
+  }
+  delete h;
+}
+
+cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_bytes, int device,
+                            cascade_handle** out) {
+  if (!cfg || !out || !d_ws) return CASCADE_ERR_INVALID_ARG;
+  *out = nullptr;
+  cascade_status st = cascade_validate_config(cfg);
+  if (st != CASCADE_OK) return st;
+  Sizes sz = compute_sizes(*cfg);
+  if (ws_bytes < sz.total || (reinterpret_cast<uintptr_t>(d_ws) % kAlign)) return CASCADE_ERR_WORKSPACE;
+  if (cudaSetDevice(device) != cudaSuccess) return CASCADE_ERR_CUDA;
+
+  cascade_handle* h = new (std::nothrow) cascade_handle();
+  if (!h) return CASCADE_ERR_INVALID_ARG;
+  h->cfg = *cfg;
+  h->device = device;
+  h->sz = sz;
+  h->alpha = cfg->sink_size;
+  h->N = cfg->num_cascades;
+  h->c = cfg->cache_size / cfg->num_cascades;
+  h->S_tot = h->alpha + cfg->cache_size;
+  h->planner.configure(h->alpha, h->N, h->c);
+  h->launches = 0;
+  h->ring_pos = 0;
+  for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
+
+  char* p = static_cast<char*>(d_ws);
+  auto take = [&](size_t n) { char* r = p; p += n; return r; };
+  h->layers.resize(cfg->num_layers);
+  for (auto& L : h->layers) {
+    L.k_raw = take(sz.k_raw); L.v = take(sz.v);
+    L.mu = reinterpret_cast<double*>(take(sz.mu));
+    L.origin = reinterpret_cast<int64_t*>(take(sz.origin));
+    L.pe = reinterpret_cast<int32_t*>(take(sz.pe));
+    L.s = reinterpret_cast<float*>(take(sz.s));
+    L.lse = reinterpret_cast<float*>(take(sz.lse));
+    L.plan = reinterpret_cast<int32_t*>(take(sz.plan));
+    L.resolved = reinterpret_cast<int32_t*>(take(sz.resolved));
+    L.q_rot = take(sz.q_rot); L.k_rot = take(sz.k_rot); L.v_chunk = take(sz.v_chunk);
+  }
+  h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
+  h->stage_q = take(sz.stage_q); h->stage_k = take(sz.stage_kv);
+  h->stage_v = take(sz.stage_kv); h->stage_out = take(sz.stage_out);
+  h->mirrors.assign(cfg->num_layers, cascade_mirror{});
+  h->m_last.assign(cfg->num_layers, 0);
+
+  bool ok = true;
+  for (int i = 0; i < kRing && ok; ++i) {
+    ok = cudaHostAlloc(reinterpret_cast<void**>(&h->pinned[i]), (size_t)sz.plan_ints * 4,
+                       cudaHostAllocDefault) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ring_ev[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+  // Empty cascades: mu = 0, origin = -1 (all bytes 0xff), scores 0.
+  for (auto& L : h->layers) {
+    ok = ok && cudaMemsetAsync(L.mu, 0, sz.mu) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.origin, 0xff, sz.origin) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.k_raw, 0, sz.k_raw) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.v, 0, sz.v) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.s, 0, sz.s) == cudaSuccess;
+  }
+  // RoPE table: (cos, sin)(pos * theta^(-2i/d)) computed in double, rounded to fp32 (Q11).
+  {
+    const int half = cfg->head_dim / 2;
+    const size_t npos = (size_t)h->S_tot + cfg->max_stride;
+    std::vector<float2> tab(npos * half);
+    for (int i = 0; i < half; ++i) {
+      const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
+      for (size_t pos = 0; pos < npos; ++pos) {
+        const double a = (double)pos * f;
+        tab[pos * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    }
+    ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(float2),
+                          cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  ok = ok && cudaDeviceSynchronize() == cudaSuccess;
+  if (!ok) { cascade_destroy(h); return CASCADE_ERR_CUDA; }
+  *out = h;
+  return CASCADE_OK;
+}
+
+int64_t cascade_launch_count(const cascade_handle* h) { return h ? h->launches : 0; }
+
+}  // extern "C"
+
+namespace {
+
+Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_t m) {
+  const cascade_config& c = h->cfg;
+  Geometry g{};
+  g.B = c.batch; g.Hq = c.num_q_heads; g.Hkv = c.num_kv_heads; g.G = g.Hq / g.Hkv; g.d = c.head_dim;
+  g.alpha = h->alpha; g.N = h->N; g.c = h->c; g.S_tot = h->S_tot;
+  g.m = m; g.t0 = mr.t; g.sink_pre = mr.sink_count;
+  int32_t base = mr.sink_count, n = mr.sink_count;
+  for (int i = h->N - 1; i >= 0; --i) { g.base_pre[i] = base; base += mr.counts[i]; }
+  for (int i = 0; i < h->N; ++i) { g.counts_pre[i] = mr.counts[i]; g.xi_pre[i] = mr.xi[i]; n += mr.counts[i]; }
+  g.n_cached = n;
+  const double scale = c.softmax_scale > 0 ? c.softmax_scale : 1.0 / std::sqrt((double)c.head_dim);
+  g.scale = (float)scale;
+  g.scale_log2 = (float)(scale * 1.4426950408889634);
+  g.decay = gamma_pow(c.ema_gamma, m);
+  return g;
+}
+
+// Builds the plan for the layer's next m tokens, uploads it (plus the EMA row weights) and
+// advances the mirror.  Returns the device plan view and phase/depth offsets via h->plan.
+cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
+                           PlanDev* pd, float** w_dev, cascade_mirror* next) {
+  *next = h->mirrors[layer];
+  h->planner.advance(*next, m, &h->plan);
+  const Plan& P = h->plan;
+  const int slot = h->ring_pos;
+  h->ring_pos = (h->ring_pos + 1) % kRing;
+  if (cudaEventSynchronize(h->ring_ev[slot]) != cudaSuccess) return CASCADE_ERR_CUDA;
+  int32_t* buf = h->pinned[slot];
+  const size_t nsel = P.sel.size(), nord = P.sel_order.size(), nmov = P.mov.size();
+  std::memcpy(buf, P.sel.data(), nsel * 4);
+  std::memcpy(buf + nsel, P.sel_order.data(), nord * 4);
+  std::memcpy(buf + nsel + nord, P.mov.data(), nmov * 4);
+  float* w = reinterpret_cast<float*>(buf + nsel + nord + nmov);
+  const double gam = h->cfg.ema_gamma;
+  for (int32_t r = 0; r < m; ++r)      // C_EMA = (1 - gamma) gamma^(m-1-r)  (Alg. 3)
+    w[r] = (float)((1.0 - gam) * gamma_pow(gam, m - 1 - r));
+  const size_t total = nsel + nord + nmov + (size_t)m;
+  LayerBufs& L = h->layers[layer];
+  if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  if (cudaEventRecord(h->ring_ev[slot], st) != cudaSuccess) return CASCADE_ERR_CUDA;
+  pd->sel = L.plan;
+  pd->sel_order = L.plan + nsel;
+  pd->mov = L.plan + nsel + nord;
+  pd->resolved = L.resolved;
+  pd->sel_cap = h->cfg.max_stride;
+  *w_dev = reinterpret_cast<float*>(L.plan + nsel + nord + nmov);
+  return CASCADE_OK;
+}
+
+template <typename T>
+void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const PlanDev& pd,
+                        const T* k, const T* v, const float* s, cudaStream_t st) {
+  const Plan& P = h->plan;
+  launch_ema_fold(g, L.mu, s, st); ++h->launches;
+  for (size_t dpt = 0; dpt + 1 < P.depth_begin.size(); ++dpt) {
+    launch_select_resolve(g, pd, P.depth_begin[dpt], P.depth_begin[dpt + 1], L.mu, s, st);
+    ++h->launches;
+  }
+  StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin};
+  for (size_t ph = 0; ph + 1 < P.phase_begin.size(); ++ph) {
+    if (P.phase_begin[ph + 1] == P.phase_begin[ph]) continue;
+    launch_moves<T>(g, pd, P.phase_begin[ph], P.phase_begin[ph + 1], sd, k, v, s, st);
+    ++h->launches;
+  }
+}
+
+template <typename T>
+cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const T* k, const T* v,
+                            int32_t m, T* out, cudaStream_t st) {
+  LayerBufs& L = h->layers[layer];
+  const Geometry g = make_geometry(h, h->mirrors[layer], m);
+  PlanDev pd;
+  float* w;
+  cascade_mirror next;
+  cascade_status rc = upload_plan(h, layer, m, st, &pd, &w, &next);
+  if (rc != CASCADE_OK) return rc;
+  T* q_rot = reinterpret_cast<T*>(L.q_rot);
+  T* k_rot = reinterpret_cast<T*>(L.k_rot);
+  T* v_chunk = reinterpret_cast<T*>(L.v_chunk);
+  launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, q_rot, k_rot,
+                      v_chunk, st);
+  launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
+  launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, w, L.s, st);
+  h->launches += 3;
+  launch_maintenance<T>(h, g, L, pd, k, v, L.s, st);
+  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  h->mirrors[layer] = next;   // commit the mirror
+  h->m_last[layer] = m;
+  return CASCADE_OK;
+}
+
+cascade_status check_call(cascade_handle* h, int32_t layer, int32_t m) {
+  if (!h) return CASCADE_ERR_INVALID_ARG;
+  if (layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (m < 1 || m > h->cfg.max_stride) return CASCADE_ERR_SHAPE;
+  return CASCADE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cascade_status cascade_prefill_stride(cascade_handle* h, int32_t layer, const void* q, const void* k,
+                                      const void* v, int32_t m, void* out, void* stream) {
+  cascade_status rc = check_call(h, layer, m);
+  if (rc != CASCADE_OK) return rc;
+  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (h->cfg.dtype == CASCADE_BF16)
+    return prefill_impl<__nv_bfloat16>(h, layer, static_cast<const __nv_bfloat16*>(q),
+                                       static_cast<const __nv_bfloat16*>(k),
+                                       static_cast<const __nv_bfloat16*>(v), m,
+                                       static_cast<__nv_bfloat16*>(out), st);
+  return prefill_impl<float>(h, layer, static_cast<const float*>(q), static_cast<const float*>(k),
+                             static_cast<const float*>(v), m, static_cast<float*>(out), st);
+}
+
+cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, const void* q,
+                                           const void* k, const void* v, int32_t m, void* out,
+                                           void* stream) {
+  cascade_status rc = check_call(h, layer, m);
+  if (rc != CASCADE_OK) return rc;
+  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = elem_size(h->cfg.dtype);
+  const size_t nq = (size_t)h->cfg.batch * m * h->cfg.num_q_heads * h->cfg.head_dim * es;
+  const size_t nk = (size_t)h->cfg.batch * m * h->cfg.num_kv_heads * h->cfg.head_dim * es;
+  if (cudaMemcpyAsync(h->stage_q, q, nq, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(h->stage_k, k, nk, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(h->stage_v, v, nk, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  rc = cascade_prefill_stride(h, layer, h->stage_q, h->stage_k, h->stage_v, m, h->stage_out, stream);
+  if (rc != CASCADE_OK) return rc;
+  if (cudaMemcpyAsync(out, h->stage_out, nq, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return CASCADE_ERR_CUDA;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,
+                              const void* v, void* out, void* stream) {
+  // q [B,Hq,d] is [B,1,Hq,d]: the m = 1 case of the strided step (Eq. 2).
+  return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
+}
+
+cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, const void* k,
+                                          const void* v, int32_t m, const float* s, void* stream) {
+  cascade_status rc = check_call(h, layer, m);
+  if (rc != CASCADE_OK) return rc;
+  if (!k || !v || !s) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerBufs& L = h->layers[layer];
+  const Geometry g = make_geometry(h, h->mirrors[layer], m);
+  PlanDev pd;
+  float* w;
+  cascade_mirror next;
+  rc = upload_plan(h, layer, m, st, &pd, &w, &next);
+  if (rc != CASCADE_OK) return rc;
+  if (h->cfg.dtype == CASCADE_BF16)
+    launch_maintenance<__nv_bfloat16>(h, g, L, pd, static_cast<const __nv_bfloat16*>(k),
+                                      static_cast<const __nv_bfloat16*>(v), s, st);
+  else
+    launch_maintenance<float>(h, g, L, pd, static_cast<const float*>(k), static_cast<const float*>(v), s, st);
+  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  h->mirrors[layer] = next;
+  h->m_last[layer] = 0;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out, int32_t* m_last,
+                                   void* stream) {
+  if (!h || !out || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  const int32_t m = h->m_last[layer];
+  if (m_last) *m_last = m;
+  if (m == 0) return CASCADE_ERR_ORDER;
+  const size_t n = (size_t)h->cfg.batch * h->cfg.num_kv_heads * (h->S_tot + m);
+  if (cudaMemcpyAsync(out, h->layers[layer].s, n * 4, cudaMemcpyDeviceToDevice,
+                      static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out, void* stream) {
+  if (!h || !out || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerBufs& L = h->layers[layer];
+  const cascade_mirror& mr = h->mirrors[layer];
+  const Geometry g = make_geometry(h, mr, 1);
+  launch_positions(g, L.pe, st);
+  ++h->launches;
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  std::memset(out, 0, sizeof(*out));
+  out->mirror = mr;
+  out->num_cascades = h->N; out->sub_cache_size = h->c; out->sink_size = h->alpha;
+  out->slots_total = h->S_tot; out->head_dim = h->cfg.head_dim; out->dtype = h->cfg.dtype;
+  out->batch = h->cfg.batch; out->num_kv_heads = h->cfg.num_kv_heads;
+  out->n_cached = g.n_cached;
+  out->k_raw = L.k_raw; out->v = L.v; out->mu = L.mu; out->origin = L.origin; out->pe = L.pe;
+  return CASCADE_OK;
+}
+
+}  // extern "C"

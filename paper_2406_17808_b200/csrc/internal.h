@@ -1,0 +1,89 @@
+// internal.h -- shared between the host control plane and the kernels (library-private).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/cascade.h"
+
+namespace cascade {
+
+// Per-call geometry of one layer's cascades, passed by value to every kernel.
+// "pre" = state before the chunk (what attention sees and what the fold uses).
+struct Geometry {
+  int32_t B, Hq, Hkv, G, d;
+  int32_t alpha, N, c, S_tot;           // S_tot = alpha + N*c
+  int32_t m;                            // chunk length
+  int64_t t0;                           // stream index of chunk row 0
+  int32_t sink_pre;                     // sink residents before the chunk
+  int32_t n_cached;                     // residents before the chunk
+  int32_t counts_pre[CASCADE_MAX_LEVELS];
+  int32_t xi_pre[CASCADE_MAX_LEVELS];
+  int32_t base_pre[CASCADE_MAX_LEVELS]; // pe of the oldest token of sub-cache i (logical order)
+  float scale;                          // softmax scale
+  float scale_log2;                     // scale * log2(e)
+  double decay;                         // g = gamma^m
+};
+
+// pe of a pre-chunk resident flat slot x (-1 if empty).  Closed form of the logical
+// order [sinks; C_N oldest..newest; ...; C_1].
+__host__ __device__ inline int32_t slot_pe(const Geometry& g, int32_t x) {
+  if (x < g.alpha) return x < g.sink_pre ? x : -1;
+  int32_t rel = x - g.alpha;
+  int32_t i = rel / g.c;               // 0-based level
+  int32_t s = rel - i * g.c;
+  int32_t cnt = g.counts_pre[i];
+  if (s >= cnt) return -1;
+  int32_t rank = (cnt == g.c) ? ((s - g.xi_pre[i] + g.c) % g.c) : s;
+  return g.base_pre[i] + rank;
+}
+
+struct Workspace;  // device carve (host side)
+
+// Schedule of one chunk, in device memory (int32):
+//   sel[3*k + {0,1,2}] = {slot, cand_ref, inc_ref}       k < n_sel
+//   sel_order[]        = select indices sorted by dependency depth
+//   mov[2*e + {0,1}]   = {dst_slot, ref}                 grouped by phase
+// A ref >= 0 is a concrete source: flat slot (< S_tot, pre-chunk occupant) or
+// chunk row (S_tot + r).  A ref < 0 is -(k+1): the winner of select k.
+struct PlanDev {
+  const int32_t* sel;
+  const int32_t* sel_order;
+  const int32_t* mov;
+  int32_t* resolved;        // [B*Hkv][sel_cap]
+  int32_t sel_cap;
+};
+
+template <typename T>
+struct StateDev {
+  T* k_raw;        // [B*Hkv][S_tot][d]
+  T* v;            // [B*Hkv][S_tot][d]
+  double* mu;      // [B*Hkv][S_tot]
+  int64_t* origin; // [B*Hkv][S_tot]
+};
+
+// ---- launchers (defined in the .cu files) --------------------------------
+template <typename T>
+void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, const T* k_raw_state,
+                      const float2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st);
+
+template <typename T>
+void launch_attn_fwd_simt(const Geometry& g, const T* q_rot, const T* k_rot, const T* v_state,
+                          const T* v_chunk, T* out, float* lse, cudaStream_t st);
+
+template <typename T>
+void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, const float* lse,
+                            const float* w, float* s, cudaStream_t st);
+
+void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t st);
+
+void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end,
+                           const double* mu, const float* s, cudaStream_t st);
+
+template <typename T>
+void launch_moves(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end, StateDev<T> st_,
+                  const T* k_in, const T* v_in, const float* s, cudaStream_t st);
+
+void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
+
+}  // namespace cascade

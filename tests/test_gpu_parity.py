@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same seeded inputs.
+
+* score injection (cascade_update_with_scores): the cascade state -- origins, pe, counts, xi,
+  the mu bit patterns and the K/V payload bits -- must be BIT-EXACT after every call.
+* end to end (cascade_prefill_stride / cascade_decode): outputs within the north-star
+  tolerance (fp32 1e-4, bf16 2e-2 max-abs), per-key mass within 1e-3 relative, and the
+  cascade contents (origins, pe, counts, xi) exact, on inputs whose selection margins the
+  oracle audits to exceed 1e-3.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.model import CascadeOracle, OracleConfig
+from paper_2406_17808_b200 import cascade as C
+from paper_2406_17808_b200.synth import CONFIGS, Synth, config_seed
+
+pytestmark = pytest.mark.gpu
+
+O_TOL = {"f32": 1e-4, "bf16": 2e-2}
+S_RTOL = 1e-3
+
+
+def _np(t):
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def _oracle_cfg(cfg: C.CascadeConfig) -> OracleConfig:
+    return OracleConfig(cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+                        cfg.sink_size, cfg.cache_size, cfg.num_cascades, gamma=cfg.ema_gamma,
+                        rope_theta=cfg.rope_theta, round_operands="bf16" if cfg.dtype == "bf16" else "")
+
+
+def _compare_state(gpu_state, orc_state, exact_mu=True, exact_payload=True, layer_meta=None):
+    o_org = orc_state["origin"]
+    g_org = gpu_state["origin"].cpu().numpy()
+    np.testing.assert_array_equal(g_org, o_org)
+    g_pe = gpu_state["pe"].cpu().numpy()
+    np.testing.assert_array_equal(np.broadcast_to(g_pe, o_org.shape), orc_state["pe"])
+    meta = orc_state["meta"][0][0]
+    assert gpu_state["t"] == meta["t"] and gpu_state["sink_count"] == meta["sink_count"]
+    assert gpu_state["counts"] == meta["counts"] and gpu_state["xi"] == meta["xi"]
+    valid = o_org >= 0
+    g_mu = gpu_state["mu"].cpu().numpy()
+    if exact_mu:
+        assert np.array_equal(g_mu.view(np.uint64)[valid], orc_state["mu"].view(np.uint64)[valid])
+    else:
+        np.testing.assert_allclose(g_mu[valid], orc_state["mu"][valid], rtol=S_RTOL, atol=1e-30)
+    if exact_payload:
+        np.testing.assert_array_equal(_np(gpu_state["k"])[valid], orc_state["k"][valid])
+        np.testing.assert_array_equal(_np(gpu_state["v"])[valid], orc_state["v"][valid])
+
+
+SMALL = [  # (alpha, N, c, B, Hkv, dtype, strides)
+    (1, 2, 2, 1, 1, "f32", [1] * 12),                  # the Appendix-A toy geometry
+    (4, 4, 16, 1, 1, "f32", [16] * 32),                # cfg1 geometry
+    (3, 3, 5, 2, 2, "bf16", [1, 2, 3, 7, 5, 11, 4, 9, 13, 6, 8, 1, 1, 12]),
+    (0, 1, 7, 1, 2, "f32", [3, 9, 14, 1, 2, 7]),       # no sinks, N = 1 (FIFO)
+    (2, 5, 3, 1, 1, "bf16", [4] * 20 + [15, 15, 16]),  # m > c: wrapped levels, dependent selects
+    (64, 4, 1024, 1, 2, "bf16", [1024] * 10),          # cfg2 geometry
+]
+
+
+@pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", SMALL)
+def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides):
+    d = 64
+    cfg = C.CascadeConfig(batch=B, num_q_heads=Hkv, num_kv_heads=Hkv, head_dim=d, sink_size=alpha,
+                          cache_size=N * c, num_cascades=N, max_stride=max(strides), dtype=dtype,
+                          ema_gamma=0.99)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    rng = np.random.default_rng(alpha * 131 + N * 17 + c)
+    torch.manual_seed(alpha * 131 + N * 17 + c)
+    tdt = cfg.torch_dtype
+    for m in strides:
+        k = torch.randn((B, m, Hkv, d), dtype=torch.float32).to(tdt)
+        v = torch.randn((B, m, Hkv, d), dtype=torch.float32).to(tdt)
+        s = rng.random((B, Hkv, cfg.s_tot + m)).astype(np.float32)
+        s[rng.random(s.shape) < 0.3] = 0.25          # ties on purpose (resident must win)
+        gpu.update_with_scores(0, k.cuda(), v.cuda(), torch.from_numpy(s).cuda())
+        orc.update_with_scores(0, _np(k), _np(v), s.astype(np.float64))
+        torch.cuda.synchronize()
+        _compare_state(gpu.state(0), orc.state(0))
+
+
+def _run_end_to_end(name, n_chunks=None, check_every=1):
+    spec = dict(CONFIGS[name])
+    cfg = C.CascadeConfig(num_layers=1, batch=spec["batch"], num_q_heads=spec["num_q_heads"],
+                          num_kv_heads=spec["num_kv_heads"], head_dim=spec["head_dim"],
+                          sink_size=spec["sink_size"], cache_size=spec["cache_size"],
+                          num_cascades=spec["num_cascades"], max_stride=spec["stride"],
+                          dtype=spec["dtype"], rope_theta=spec["rope_theta"])
+    k_idx = int(name[3])
+    syn = Synth(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, config_seed(k_idx),
+                eps=spec["eps"], dtype=cfg.torch_dtype)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    m = spec["stride"]
+    total = spec["tokens"] if n_chunks is None else n_chunks * m
+    worst_o, worst_s = 0.0, 0.0
+    for ci, start in enumerate(range(0, total, m)):
+        q, k, v = syn.chunk(start, m)
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        s_gpu = gpu.last_scores(0)
+        O_ref, s_ref = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        torch.cuda.synchronize()
+        err = np.abs(_np(out) - O_ref).max()
+        worst_o = max(worst_o, err)
+        assert err <= O_TOL[cfg.dtype], (ci, err)
+        sg = _np(s_gpu)
+        np.testing.assert_allclose(sg, s_ref, rtol=S_RTOL, atol=1e-30)
+        big = s_ref > 1e-30
+        worst_s = max(worst_s, float(np.max(np.abs(sg[big] - s_ref[big]) / s_ref[big])))
+        if ci % check_every == 0:
+            _compare_state(gpu.state(0), orc.state(0), exact_mu=False, exact_payload=True)
+    margins = orc.select_margins()
+    assert margins.size == 0 or margins.min() > 1e-3, margins.min()
+    return worst_o, worst_s, margins
+
+
+def test_cfg1_toy_end_to_end_fp32():
+    worst_o, worst_s, margins = _run_end_to_end("cfg1_toy")
+    assert margins.size > 0          # selections happened
+    print(f"cfg1: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
+
+
+def test_cfg2_first_chunks_end_to_end_bf16():
+    worst_o, worst_s, margins = _run_end_to_end("cfg2_llama8b_4k", n_chunks=6, check_every=2)
+    print(f"cfg2[0:6]: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e}")
+
+
+@pytest.mark.slow
+def test_cfg2_full_end_to_end_bf16():
+    worst_o, worst_s, margins = _run_end_to_end("cfg2_llama8b_4k", check_every=8)
+    assert margins.size > 0
+    print(f"cfg2: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
+
+
+def test_decode_matches_oracle():
+    """Eq. 2 steps after a short prefill, bf16, GQA 4:1, B = 3."""
+    cfg = C.CascadeConfig(batch=3, num_q_heads=8, num_kv_heads=2, head_dim=128, sink_size=4,
+                          cache_size=64, num_cascades=4, max_stride=32, dtype="bf16")
+    syn = Synth(3, 8, 2, 128, seed=77)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    for start in range(0, 96, 32):
+        q, k, v = syn.chunk(start, 32)
+        gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        orc.prefill_stride(0, _np(q), _np(k), _np(v))
+    for step in range(40):
+        q, k, v = syn.chunk(96 + step, 1)
+        out = gpu.decode(0, q[:, 0].contiguous().cuda(), k[:, 0].contiguous().cuda(),
+                         v[:, 0].contiguous().cuda())
+        O_ref, s_ref = orc.decode(0, _np(q[:, 0]), _np(k[:, 0]), _np(v[:, 0]))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL["bf16"]
+        np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+    _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
+
+
+def test_errors_leave_state_untouched():
+    cfg = C.CascadeConfig(batch=1, num_q_heads=4, num_kv_heads=2, head_dim=64, sink_size=2,
+                          cache_size=8, num_cascades=2, max_stride=4, dtype="bf16")
+    gpu = C.Cascade(cfg)
+    q = torch.zeros((1, 5, 4, 64), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((1, 5, 2, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(C.CascadeError) as e:
+        gpu.prefill_stride(0, q, k, k)              # m = 5 > max_stride
+    assert e.value.code == -3
+    with pytest.raises(C.CascadeError):
+        gpu.prefill_stride(3, q[:, :2].contiguous(), k[:, :2].contiguous(), k[:, :2].contiguous())
+    st = gpu.state(0)
+    assert st["t"] == 0 and st["n_cached"] == 0

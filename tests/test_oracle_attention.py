@@ -239,3 +239,15 @@ def test_decode_is_prefill_with_stride_one_and_eq2():
     # all 6 tokens resident (5 + new): s over [cache(5) | new] equals (1-gamma) max_h P
     s_flat = s[0, 0]
     np.testing.assert_allclose(np.sort(s_flat[s_flat > 0]), np.sort(0.1 * P.max(0)), rtol=1e-13)
+
+
+def test_round_bf16_against_torch_and_exact_values():
+    """RNE to bfloat16: exact on representable values, agrees with torch's conversion."""
+    from oracle.attention import round_bf16
+    exact = np.array([0.0, 1.0, -2.5, 0.125, 31.875, 64.0, 2.0 ** -100])
+    np.testing.assert_array_equal(round_bf16(exact), exact)
+    assert round_bf16(np.array([1.0 + 2.0 ** -8]))[0] == 1.0             # tie -> even (1.0)
+    assert round_bf16(np.array([1.0 + 3 * 2.0 ** -8]))[0] == 1.0 + 2.0 ** -6  # tie -> even (up)
+    x = np.random.default_rng(9).standard_normal(100000) * 10
+    ref = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(round_bf16(x), ref)
