@@ -190,9 +190,24 @@ cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out,
 cascade_status cascade_mirror_advance(const cascade_config* cfg, cascade_mirror* mirror,
                                       int32_t m, int32_t* pe_out, int64_t* ops_out);
 
+/* Empties the cascades of one layer (mu = 0, origin = -1, counters 0) with
+ * stream-ordered memsets; K/V payloads are left as they are (unreachable). */
+cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream);
+
 /* Number of kernel launches issued by this handle since init (for the bench's
  * gpu_launches count). */
 int64_t cascade_launch_count(const cascade_handle* h);
+
+/* Kernel-class timing with CUDA events recorded on the launch stream around each
+ * launch group (off by default; enabling adds event records, no synchronisation).
+ * Classes: 0 rope/prep, 1 attention pass 1, 2 score pass 2, 3 maintenance (fold +
+ * resolve + moves), 4 decode attention.  cascade_profile_read synchronises the
+ * recorded events and returns, per class, the summed milliseconds, the number of
+ * launch groups and the summed algorithmic work (flops for 1/2/4 as 4*d per visible
+ * (query, key) pair; bytes for 0/3 as documented in DESIGN.md), then clears them. */
+#define CASCADE_PROFILE_CLASSES 5
+cascade_status cascade_profile_enable(cascade_handle* h, int32_t enable);
+cascade_status cascade_profile_read(cascade_handle* h, double* ms, int64_t* count, double* work);
 
 #ifdef __cplusplus
 }

@@ -81,6 +81,9 @@ def lib():
             "cascade_last_scores": (i32, [vp, i32, vp, ctypes.POINTER(i32), vp]),
             "cascade_mirror_advance": (i32, [cfgp, ctypes.POINTER(Mirror), i32, vp, vp]),
             "cascade_launch_count": (ctypes.c_int64, [vp]),
+            "cascade_reset": (i32, [vp, i32, vp]),
+            "cascade_profile_enable": (i32, [vp, i32]),
+            "cascade_profile_read": (i32, [vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -94,7 +97,8 @@ EXPORTED = ["cascade_status_string", "cascade_validate_config", "cascade_workspa
             "cascade_init", "cascade_destroy", "cascade_prefill_stride",
             "cascade_prefill_stride_host", "cascade_decode", "cascade_state",
             "cascade_update_with_scores", "cascade_last_scores", "cascade_mirror_advance",
-            "cascade_launch_count"]
+            "cascade_launch_count", "cascade_reset", "cascade_profile_enable",
+            "cascade_profile_read"]
 
 
 @dataclass
@@ -284,3 +288,22 @@ class Cascade:
 
     def launch_count(self) -> int:
         return int(lib().cascade_launch_count(self._h))
+
+    def reset(self, layer: int, stream=None) -> None:
+        _check(lib().cascade_reset(self._h, layer, _stream(stream)), "cascade_reset")
+
+    def profile_enable(self, on: bool = True) -> None:
+        _check(lib().cascade_profile_enable(self._h, 1 if on else 0), "cascade_profile_enable")
+
+    PROFILE_CLASSES = ("prep", "attn_fwd", "attn_score", "maintenance", "decode_attn")
+
+    def profile_read(self) -> dict:
+        """{class: (ms_total, launch_groups, algorithmic_work)} since the last read."""
+        import numpy as np
+        ms = np.zeros(5, dtype=np.float64)
+        cnt = np.zeros(5, dtype=np.int64)
+        work = np.zeros(5, dtype=np.float64)
+        _check(lib().cascade_profile_read(self._h, ms.ctypes.data_as(ctypes.c_void_p),
+                                          cnt.ctypes.data_as(ctypes.c_void_p),
+                                          work.ctypes.data_as(ctypes.c_void_p)), "cascade_profile_read")
+        return {n: (float(ms[i]), int(cnt[i]), float(work[i])) for i, n in enumerate(self.PROFILE_CLASSES)}

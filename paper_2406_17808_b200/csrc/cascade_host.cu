@@ -88,7 +88,38 @@ struct cascade_handle {
   cudaEvent_t ring_ev[kRing];
   int ring_pos;
   int64_t launches;
+  // profiling (cascade_profile_*)
+  bool profiling;
+  struct Rec { cudaEvent_t a, b; double work; };
+  std::vector<Rec> recs[CASCADE_PROFILE_CLASSES];
+  std::vector<cudaEvent_t> ev_pool;
 };
+
+namespace {
+
+cudaEvent_t pool_event(cascade_handle* h) {
+  if (!h->ev_pool.empty()) { cudaEvent_t e = h->ev_pool.back(); h->ev_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII-ish scope: records a start event on construction and an end event on finish().
+struct ProfScope {
+  cascade_handle* h; int cls; cudaStream_t st; cudaEvent_t a = nullptr;
+  ProfScope(cascade_handle* h_, int cls_, cudaStream_t st_) : h(h_), cls(cls_), st(st_) {
+    if (h->profiling) { a = pool_event(h); cudaEventRecord(a, st); }
+  }
+  void finish(double work) {
+    if (!a) return;
+    cudaEvent_t b = pool_event(h);
+    cudaEventRecord(b, st);
+    h->recs[cls].push_back({a, b, work});
+    a = nullptr;
+  }
+};
+
+}  // namespace
 
 extern "C" {
 
@@ -153,6 +184,9 @@ cascade_status cascade_mirror_advance(const cascade_config* cfg, cascade_mirror*
 
 void cascade_destroy(cascade_handle* h) {
   if (!h) return;
+  for (auto& v : h->recs)
+    for (auto& r : v) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < kRing; ++i) {
     if (h->ring_ev[i]) cudaEventDestroy(h->ring_ev[i]);
     if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
@@ -182,6 +216,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->planner.configure(h->alpha, h->N, h->c);
   h->launches = 0;
   h->ring_pos = 0;
+  h->profiling = false;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
 
   char* p = static_cast<char*>(d_ws);
@@ -299,6 +334,7 @@ template <typename T>
 void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const PlanDev& pd,
                         const T* k, const T* v, const float* s, cudaStream_t st) {
   const Plan& P = h->plan;
+  ProfScope ps(h, 3, st);
   launch_ema_fold(g, L.mu, s, st); ++h->launches;
   for (size_t dpt = 0; dpt + 1 < P.depth_begin.size(); ++dpt) {
     launch_select_resolve(g, pd, P.depth_begin[dpt], P.depth_begin[dpt + 1], L.mu, s, st);
@@ -310,6 +346,11 @@ void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
     launch_moves<T>(g, pd, P.phase_begin[ph], P.phase_begin[ph + 1], sd, k, v, s, st);
     ++h->launches;
   }
+  // algorithmic bytes: EMA 20 B per resident (mu r/w + s), each final row write moves
+  // K, V, mu, origin once (read + write)
+  const double bg = (double)g.B * g.Hkv;
+  const double row = 2.0 * (2.0 * g.d * sizeof(T) + 16.0);
+  ps.finish(bg * (20.0 * g.n_cached + row * (double)(P.mov.size() / 2)));
 }
 
 template <typename T>
@@ -325,10 +366,25 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
   T* q_rot = reinterpret_cast<T*>(L.q_rot);
   T* k_rot = reinterpret_cast<T*>(L.k_rot);
   T* v_chunk = reinterpret_cast<T*>(L.v_chunk);
-  launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, q_rot, k_rot,
-                      v_chunk, st);
-  launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
-  launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, w, L.s, st);
+  const double es = sizeof(T);
+  const double pairs = (double)g.B * g.Hq * ((double)m * g.n_cached + 0.5 * (double)m * (m + 1));
+  const double useful = 4.0 * g.d * pairs;
+  {
+    ProfScope ps(h, 0, st);
+    launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, q_rot, k_rot,
+                        v_chunk, st);
+    ps.finish(2.0 * es * g.d * ((double)g.B * g.Hq * m + (double)g.B * g.Hkv * (g.n_cached + 2.0 * m)));
+  }
+  {
+    ProfScope ps(h, 1, st);
+    launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
+    ps.finish(useful);
+  }
+  {
+    ProfScope ps(h, 2, st);
+    launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, w, L.s, st);
+    ps.finish(useful);
+  }
   h->launches += 3;
   launch_maintenance<T>(h, g, L, pd, k, v, L.s, st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
@@ -425,6 +481,40 @@ cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out,
   if (cudaMemcpyAsync(out, h->layers[layer].s, n * 4, cudaMemcpyDeviceToDevice,
                       static_cast<cudaStream_t>(stream)) != cudaSuccess)
     return CASCADE_ERR_CUDA;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
+  if (!h || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerBufs& L = h->layers[layer];
+  if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
+      cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  h->mirrors[layer] = cascade_mirror{};
+  h->m_last[layer] = 0;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_profile_enable(cascade_handle* h, int32_t enable) {
+  if (!h) return CASCADE_ERR_INVALID_ARG;
+  h->profiling = enable != 0;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_profile_read(cascade_handle* h, double* ms, int64_t* count, double* work) {
+  if (!h || !ms || !count || !work) return CASCADE_ERR_INVALID_ARG;
+  for (int c = 0; c < CASCADE_PROFILE_CLASSES; ++c) {
+    ms[c] = 0; count[c] = 0; work[c] = 0;
+    for (auto& r : h->recs[c]) {
+      float t = 0.f;
+      if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+        return CASCADE_ERR_CUDA;
+      ms[c] += t; count[c] += 1; work[c] += r.work;
+      h->ev_pool.push_back(r.a); h->ev_pool.push_back(r.b);
+    }
+    h->recs[c].clear();
+  }
   return CASCADE_OK;
 }
 
