@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -30,7 +31,38 @@ struct LayerBufs {
   // per-call scratch (per layer so layers may run on different streams)
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
+  CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
 };
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D bf16 row-major [rows][d] map with 64 x 128 boxes and 128-byte swizzle (the UMMA K-major /
+// MN-major SW128 canonical layouts).
+bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {d, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
@@ -53,8 +85,9 @@ Sizes compute_sizes(const cascade_config& c) {
   z.pe = align_up(S * 4);
   z.s = align_up(B * Hk * (S + M) * 4);
   z.lse = align_up(B * Hq * M * 4);
-  // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats)
-  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + M + 16);
+  // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
+  // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 2 * (S / 128 + N + 2) + 16);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -252,6 +285,19 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     ok = ok && cudaMemsetAsync(L.k_raw, 0, sz.k_raw) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.v, 0, sz.v) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.s, 0, sz.s) == cudaSuccess;
+    // scratch read by masked lanes of the MMAs must hold finite values (0 * NaN = NaN)
+    ok = ok && cudaMemsetAsync(L.q_rot, 0, sz.q_rot) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.k_rot, 0, sz.k_rot) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.v_chunk, 0, sz.v_chunk) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.lse, 0, sz.lse) == cudaSuccess;
+    if (cfg->dtype == CASCADE_BF16) {
+      const uint64_t B = cfg->batch, Hq = cfg->num_q_heads, Hk = cfg->num_kv_heads, M = cfg->max_stride;
+      const uint32_t d = cfg->head_dim;
+      ok = ok && make_map(&L.tm_q, L.q_rot, B * Hq * M, d) &&
+           make_map(&L.tm_k, L.k_rot, B * Hk * ((uint64_t)h->S_tot + M), d) &&
+           make_map(&L.tm_vs, L.v, B * Hk * (uint64_t)h->S_tot, d) &&
+           make_map(&L.tm_vc, L.v_chunk, B * Hk * M, d);
+    }
   }
   // RoPE table: (cos, sin)(pos * theta^(-2i/d)) computed in double, rounded to fp32 (Q11).
   {
@@ -285,7 +331,7 @@ Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_
   Geometry g{};
   g.B = c.batch; g.Hq = c.num_q_heads; g.Hkv = c.num_kv_heads; g.G = g.Hq / g.Hkv; g.d = c.head_dim;
   g.alpha = h->alpha; g.N = h->N; g.c = h->c; g.S_tot = h->S_tot;
-  g.m = m; g.t0 = mr.t; g.sink_pre = mr.sink_count;
+  g.m = m; g.ldc = c.max_stride; g.t0 = mr.t; g.sink_pre = mr.sink_count;
   int32_t base = mr.sink_count, n = mr.sink_count;
   for (int i = h->N - 1; i >= 0; --i) { g.base_pre[i] = base; base += mr.counts[i]; }
   for (int i = 0; i < h->N; ++i) { g.counts_pre[i] = mr.counts[i]; g.xi_pre[i] = mr.xi[i]; n += mr.counts[i]; }
@@ -299,9 +345,19 @@ Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_
 
 // Builds the plan for the layer's next m tokens, uploads it (plus the EMA row weights) and
 // advances the mirror.  Returns the device plan view and phase/depth offsets via h->plan.
+struct Upload {
+  PlanDev pd;
+  const float* w;        // [m] EMA row weights (1 - gamma) gamma^(m-1-r)
+  const float* log2w;    // [m] their log2 (-inf when w == 0)
+  const int2* tiles;     // resident key tiles (start slot, valid length)
+  int32_t n_tiles;
+};
+
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
-                           PlanDev* pd, float** w_dev, cascade_mirror* next) {
-  *next = h->mirrors[layer];
+                           Upload* up, cascade_mirror* next) {
+  PlanDev* pd = &up->pd;
+  const cascade_mirror pre = h->mirrors[layer];
+  *next = pre;
   h->planner.advance(*next, m, &h->plan);
   const Plan& P = h->plan;
   const int slot = h->ring_pos;
@@ -313,10 +369,26 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   std::memcpy(buf + nsel, P.sel_order.data(), nord * 4);
   std::memcpy(buf + nsel + nord, P.mov.data(), nmov * 4);
   float* w = reinterpret_cast<float*>(buf + nsel + nord + nmov);
+  float* lw = w + m;
   const double gam = h->cfg.ema_gamma;
-  for (int32_t r = 0; r < m; ++r)      // C_EMA = (1 - gamma) gamma^(m-1-r)  (Alg. 3)
-    w[r] = (float)((1.0 - gam) * gamma_pow(gam, m - 1 - r));
-  const size_t total = nsel + nord + nmov + (size_t)m;
+  for (int32_t r = 0; r < m; ++r) {    // C_EMA = (1 - gamma) gamma^(m-1-r)  (Alg. 3)
+    const double wr = (1.0 - gam) * gamma_pow(gam, m - 1 - r);
+    w[r] = (float)wr;
+    lw[r] = wr > 0 ? (float)std::log2(wr) : -INFINITY;
+  }
+  // resident key tiles: valid runs (sinks, then sub-caches 1..N) cut into 128-slot tiles
+  int32_t* tiles = reinterpret_cast<int32_t*>(lw + m);
+  int32_t nt = 0;
+  auto add_run = [&](int32_t beg, int32_t len) {
+    for (int32_t o = 0; o < len; o += 128) {
+      tiles[2 * nt] = beg + o;
+      tiles[2 * nt + 1] = std::min(128, len - o);
+      ++nt;
+    }
+  };
+  add_run(0, pre.sink_count);
+  for (int32_t i = 0; i < h->N; ++i) add_run(h->alpha + i * h->c, pre.counts[i]);
+  const size_t total = nsel + nord + nmov + 2 * (size_t)m + 2 * (size_t)nt;
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -326,7 +398,10 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   pd->mov = L.plan + nsel + nord;
   pd->resolved = L.resolved;
   pd->sel_cap = h->cfg.max_stride;
-  *w_dev = reinterpret_cast<float*>(L.plan + nsel + nord + nmov);
+  up->w = reinterpret_cast<const float*>(L.plan + nsel + nord + nmov);
+  up->log2w = up->w + m;
+  up->tiles = reinterpret_cast<const int2*>(up->log2w + m);
+  up->n_tiles = nt;
   return CASCADE_OK;
 }
 
@@ -358,11 +433,11 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
                             int32_t m, T* out, cudaStream_t st) {
   LayerBufs& L = h->layers[layer];
   const Geometry g = make_geometry(h, h->mirrors[layer], m);
-  PlanDev pd;
-  float* w;
+  Upload up;
   cascade_mirror next;
-  cascade_status rc = upload_plan(h, layer, m, st, &pd, &w, &next);
+  cascade_status rc = upload_plan(h, layer, m, st, &up, &next);
   if (rc != CASCADE_OK) return rc;
+  const PlanDev& pd = up.pd;
   T* q_rot = reinterpret_cast<T*>(L.q_rot);
   T* k_rot = reinterpret_cast<T*>(L.k_rot);
   T* v_chunk = reinterpret_cast<T*>(L.v_chunk);
@@ -375,15 +450,35 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
                         v_chunk, st);
     ps.finish(2.0 * es * g.d * ((double)g.B * g.Hq * m + (double)g.B * g.Hkv * (g.n_cached + 2.0 * m)));
   }
-  {
-    ProfScope ps(h, 1, st);
-    launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
-    ps.finish(useful);
-  }
-  {
-    ProfScope ps(h, 2, st);
-    launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, w, L.s, st);
-    ps.finish(useful);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    // tcgen05 path: pass 1 (O, LSE) then the key-stationary exact-mass pass 2
+    TcParams tp{};
+    tp.B = g.B; tp.Hq = g.Hq; tp.Hkv = g.Hkv; tp.G = g.G; tp.m = m; tp.M = g.ldc; tp.S_tot = g.S_tot;
+    tp.scale_log2 = g.scale_log2;
+    tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
+    tp.out = out; tp.lse2 = L.lse; tp.log2w = up.log2w; tp.s = L.s;
+    cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
+    {
+      ProfScope ps(h, 1, st);
+      launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
+      ps.finish(useful);
+    }
+    {
+      ProfScope ps(h, 2, st);
+      launch_attn_score_tc(tp, L.tm_q, L.tm_k, g.d, st);
+      ps.finish(useful);
+    }
+  } else {
+    {
+      ProfScope ps(h, 1, st);
+      launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
+      ps.finish(useful);
+    }
+    {
+      ProfScope ps(h, 2, st);
+      launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, up.w, L.s, st);
+      ps.finish(useful);
+    }
   }
   h->launches += 3;
   launch_maintenance<T>(h, g, L, pd, k, v, L.s, st);
@@ -455,11 +550,11 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   const Geometry g = make_geometry(h, h->mirrors[layer], m);
-  PlanDev pd;
-  float* w;
+  Upload up;
   cascade_mirror next;
-  rc = upload_plan(h, layer, m, st, &pd, &w, &next);
+  rc = upload_plan(h, layer, m, st, &up, &next);
   if (rc != CASCADE_OK) return rc;
+  const PlanDev& pd = up.pd;
   if (h->cfg.dtype == CASCADE_BF16)
     launch_maintenance<__nv_bfloat16>(h, g, L, pd, static_cast<const __nv_bfloat16*>(k),
                                       static_cast<const __nv_bfloat16*>(v), s, st);

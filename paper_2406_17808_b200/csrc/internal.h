@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/cascade.h"
@@ -14,6 +16,7 @@ struct Geometry {
   int32_t B, Hq, Hkv, G, d;
   int32_t alpha, N, c, S_tot;           // S_tot = alpha + N*c
   int32_t m;                            // chunk length
+  int32_t ldc;                          // row capacity of chunk-space scratch (max_stride)
   int64_t t0;                           // stream index of chunk row 0
   int32_t sink_pre;                     // sink residents before the chunk
   int32_t n_cached;                     // residents before the chunk
@@ -85,5 +88,23 @@ void launch_moves(const Geometry& g, const PlanDev& p, int32_t begin, int32_t en
                   const T* k_in, const T* v_in, const float* s, cudaStream_t st);
 
 void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
+
+// tcgen05 attention (k_attn_tc.cu)
+struct TcParams {
+  int32_t B, Hq, Hkv, G, m, M, S_tot;
+  float scale_log2;
+  int32_t n_res_tiles;
+  const int2* res_tiles;        // (start slot, valid length) of each resident key tile
+  __nv_bfloat16* out;           // [B][m][Hq][D]
+  float* lse2;                  // [B][Hq][M]  log2-domain LSE of scale*log2e*S
+  const float* log2w;           // [m]  log2 of the EMA row weights
+  float* s;                     // [B*Hkv][S_tot + m]
+};
+size_t attn_fwd_tc_smem(int d);
+size_t attn_score_tc_smem(int d);
+void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                        const CUtensorMap& tvs, const CUtensorMap& tvc, int d, cudaStream_t st);
+void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, int d,
+                          cudaStream_t st);
 
 }  // namespace cascade

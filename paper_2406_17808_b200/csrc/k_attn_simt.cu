@@ -32,12 +32,12 @@ __global__ void attn_fwd_simt_kernel(Geometry g, const T* __restrict__ q_rot,
   const long long bg = (long long)b * g.Hkv + gg;
 
   float qv[E], o[E];
-  const T* qp = q_rot + warp * D;
+  const T* qp = q_rot + (((long long)b * g.Hq + h) * g.ldc + r) * D;
 #pragma unroll
   for (int e = 0; e < E; ++e) { qv[e] = to_f(qp[lane + 32 * e]); o[e] = 0.f; }
   float mrun = -INFINITY, l = 0.f;
 
-  const T* kbase = k_rot + bg * (long long)(g.S_tot + g.m) * D;
+  const T* kbase = k_rot + bg * (long long)(g.S_tot + g.ldc) * D;
   auto visit = [&](const T* kp, const T* vp) {
     float part = 0.f;
 #pragma unroll
@@ -58,13 +58,13 @@ __global__ void attn_fwd_simt_kernel(Geometry g, const T* __restrict__ q_rot,
     for (int x = beg[j]; x < beg[j] + len[j]; ++x)
       visit(kbase + (long long)x * D, v_state + (bg * g.S_tot + x) * D);
   for (int rr = 0; rr <= r; ++rr)
-    visit(kbase + (long long)(g.S_tot + rr) * D, v_chunk + (bg * g.m + rr) * D);
+    visit(kbase + (long long)(g.S_tot + rr) * D, v_chunk + (bg * g.ldc + rr) * D);
 
   const float inv = 1.f / l;
   T* op = out + (((long long)b * g.m + r) * g.Hq + h) * D;
 #pragma unroll
   for (int e = 0; e < E; ++e) op[lane + 32 * e] = from_f<T>(o[e] * inv);
-  if (lane == 0) lse[((long long)b * g.Hq + h) * g.m + r] = mrun + logf(l);
+  if (lane == 0) lse[((long long)b * g.Hq + h) * g.ldc + r] = mrun + logf(l);
 }
 
 template <typename T, int D>
@@ -89,15 +89,15 @@ __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
     r_lo = x - g.S_tot;
   }
   float kv[E];
-  const T* kp = k_rot + warp * D;
+  const T* kp = k_rot + (bg * (g.S_tot + g.ldc) + x) * D;
 #pragma unroll
   for (int e = 0; e < E; ++e) kv[e] = to_f(kp[lane + 32 * e]);
 
   float best = 0.f;
   for (int j = 0; j < g.G; ++j) {
     const int h = gg * g.G + j;
-    const T* qb = q_rot + ((long long)b * g.Hq + h) * g.m * D;
-    const float* lb = lse + ((long long)b * g.Hq + h) * g.m;
+    const T* qb = q_rot + ((long long)b * g.Hq + h) * g.ldc * D;
+    const float* lb = lse + ((long long)b * g.Hq + h) * g.ldc;
     float acc = 0.f;
     for (int r = r_lo; r < g.m; ++r) {
       float part = 0.f;

@@ -1,11 +1,11 @@
 // k_prep.cu -- RoPE by cache rank + layout prep for the attention passes.
 //
 // Writes, for one layer and one chunk:
-//   q_rot  [B][Hq][m][d]          chunk queries rotated to pe = n_cached + r
-//   k_rot  [B][Hkv][S_tot + m][d] resident keys (flat slot order) rotated to their
+//   q_rot  [B][Hq][ldc][d]        chunk queries rotated to pe = n_cached + r
+//   k_rot  [B][Hkv][S_tot + ldc][d] resident keys (flat slot order) rotated to their
 //                                 pre-chunk rank pe (closed form, slot_pe), and chunk
 //                                 keys at rows S_tot + r rotated to n_cached + r
-//   v_chunk[B][Hkv][m][d]         chunk values, head-major
+//   v_chunk[B][Hkv][ldc][d]       chunk values, head-major
 // Keys are cached pre-RoPE (Q11) because ranks change every chunk.  cos/sin come
 // from a table built on the host in float64 and rounded to fp32 (rope_tab[pos][i]).
 // HBM-bound elementwise work: one thread per rotate-half pair, coalesced along d.
@@ -34,7 +34,7 @@ __global__ void rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* _
       const T* src = q + (((long long)b * g.m + r) * g.Hq + h) * g.d;
       float2 cs = tab[(long long)(g.n_cached + r) * half + i];
       float x1 = to_f(src[i]), x2 = to_f(src[i + half]);
-      T* dst = q_rot + row * g.d;
+      T* dst = q_rot + (bh * g.ldc + r) * g.d;
       dst[i] = from_f<T>(x1 * cs.x - x2 * cs.y);
       dst[i + half] = from_f<T>(x2 * cs.x + x1 * cs.y);
       continue;
@@ -58,7 +58,7 @@ __global__ void rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* _
       }
       float2 cs = tab[(long long)pe * half + i];
       float x1 = to_f(src[i]), x2 = to_f(src[i + half]);
-      T* dst = k_rot + row * g.d;
+      T* dst = k_rot + (bg * (g.S_tot + g.ldc) + x) * g.d;
       dst[i] = from_f<T>(x1 * cs.x - x2 * cs.y);
       dst[i + half] = from_f<T>(x2 * cs.x + x1 * cs.y);
       continue;
@@ -69,7 +69,7 @@ __global__ void rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* _
       long long bg = row / g.m;
       int gg = (int)(bg % g.Hkv), b = (int)(bg / g.Hkv);
       const T* src = v + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-      T* dst = v_chunk + row * g.d;
+      T* dst = v_chunk + (bg * g.ldc + r) * g.d;
       dst[i] = src[i];
       dst[i + half] = src[i + half];
     }
