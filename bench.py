@@ -38,6 +38,13 @@ sys.path.insert(0, ROOT)
 METRIC = "prefill tok/s at 1M ctx, 65K cascade cache; decode tok/s; % TC/HBM peak"
 
 
+T_START = time.time()
+
+
+def log(msg):
+    print(f"[bench {time.time() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -281,6 +288,7 @@ def main():
         Q[c].copy_(q[:, :, rank * hq:(rank + 1) * hq])
         K[c].copy_(k[:, :, rank * hk:(rank + 1) * hk])
         V[c].copy_(v[:, :, rank * hk:(rank + 1) * hk])
+    log(f"inputs ready: {nchunks} chunks of {m}")
     O = torch.empty_like(Q)
     O_full = torch.empty((nchunks, world, B, m, hq, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
     comm = torch.cuda.Stream() if world > 1 else None
@@ -300,9 +308,10 @@ def main():
         if world > 1:
             main_stream.wait_stream(comm)
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        log(f"warmup step {i} done")
     if world > 1:
         dist.barrier()
 
@@ -323,6 +332,7 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    log(f"timed {args.steps} steps: {ms:.1f} ms")
     launches = cas.launch_count() - n0
     prof = cas.profile_read()
     cas.profile_enable(False)
@@ -372,6 +382,7 @@ def main():
 
     # ---- e2e: host (pinned) buffers through cascade_prefill_stride_host ----
     if not args.no_e2e:
+        log("e2e start")
         Qh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
         Kh = torch.empty(K.shape, dtype=K.dtype, pin_memory=True)
         Vh = torch.empty(V.shape, dtype=V.dtype, pin_memory=True)
@@ -400,11 +411,13 @@ def main():
 
     del Q, K, V, O, O_full
     torch.cuda.empty_cache()
+    log("decode start")
     if rank == 0 and not args.no_decode and world == 1:
         try:
             result["decode"] = decode_bench(args, local, dict(CONFIGS["cfg4_decode"]), peaks)
         except Exception as e:   # reported, never hidden
             result["decode"] = {"error": repr(e)}
+    log("cpu baseline start")
     if rank == 0 and not args.no_cpu:
         secs, pairs, toks, cores = oracle_sample(spec)
         total_pairs = host_pairs(spec, Hq)

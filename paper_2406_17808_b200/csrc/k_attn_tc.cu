@@ -183,9 +183,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       if (j >= 1) {
         tc::mbar_wait(pv_done, (j - 1) & 1);              // O current, P buffer free
         tc::tc_fence_after();
-        if (mx > m_used + 8.f) {                          // lazy rescale of the O row
-          const float f = tc::fast_exp2(m_used - mx);
-          l *= f;
+        // Lazy rescale of the O row when its max grew by more than 2^8.  tcgen05.ld/st are
+        // warp-collective (.sync.aligned), so the whole warp takes the branch if any row needs it.
+        const bool need = mx > m_used + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float f = need ? tc::fast_exp2(m_used - mx) : 1.f;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
@@ -196,7 +198,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             tc::tmem_st32(tO + lane_off + c * 32, o);
           }
           tc::tmem_wait_st();
-          m_used = mx;
+          if (need) { l *= f; m_used = mx; }
         }
       } else {
         m_used = mx;
