@@ -84,7 +84,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.origin = z.mu;
   z.pe = align_up(S * 4);
   z.s = align_up(B * Hk * (S + M) * 4);
-  z.lse = align_up(B * Hq * M * 4);
+  z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 2 * (S / 128 + N + 2) + 16);
@@ -454,9 +454,10 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     // tcgen05 path: pass 1 (O, LSE) then the key-stationary exact-mass pass 2
     TcParams tp{};
     tp.B = g.B; tp.Hq = g.Hq; tp.Hkv = g.Hkv; tp.G = g.G; tp.m = m; tp.M = g.ldc; tp.S_tot = g.S_tot;
+    tp.Mb = (g.ldc + 127) / 128 * 128;
     tp.scale_log2 = g.scale_log2;
     tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
-    tp.out = out; tp.lse2 = L.lse; tp.log2w = up.log2w; tp.s = L.s;
+    tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);

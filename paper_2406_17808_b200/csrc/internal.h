@@ -92,16 +92,18 @@ void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
 // tcgen05 attention (k_attn_tc.cu)
 struct TcParams {
   int32_t B, Hq, Hkv, G, m, M, S_tot;
+  int32_t Mb;                   // row stride of qbias: max_stride rounded up to 128
   float scale_log2;
   int32_t n_res_tiles;
   const int2* res_tiles;        // (start slot, valid length) of each resident key tile
   __nv_bfloat16* out;           // [B][m][Hq][D]
-  float* lse2;                  // [B][Hq][M]  log2-domain LSE of scale*log2e*S
+  float* qbias;                 // [B][Hq][Mb] lse2 - log2(w_r): log2-domain LSE of scale*log2e*S
+                                //             minus the EMA row weight (+inf past m)
   const float* log2w;           // [m]  log2 of the EMA row weights
   float* s;                     // [B*Hkv][S_tot + m]
 };
 size_t attn_fwd_tc_smem(int d);
-size_t attn_score_tc_smem(int d);
+size_t attn_score_tc_smem(int d, int G);
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                         const CUtensorMap& tvs, const CUtensorMap& tvc, int d, cudaStream_t st);
 void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, int d,

@@ -36,7 +36,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   constexpr int KB = D / 64;                   // 64-element K blocks of a row
   constexpr int kStages = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                                   // KB blocks
   uint8_t* sP = sQ + KB * kTileBytes;                   // 2 blocks (128 keys)
   uint8_t* sK = sP + 2 * kTileBytes;                    // kStages x KB blocks
@@ -174,12 +174,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         const int k0 = (j - p.n_res_tiles) * 128;
         lim = min(qi - k0 + 1, p.m - k0);
       }
-      float mx = -INFINITY;
+      // row max over raw S (scale > 0), masking only on the (few) partial tiles
+      float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+      if (lim < 128) {
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        x[c] = c < lim ? x[c] * p.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, x[c]);
+        for (int c = 0; c < 128; ++c) x[c] = c < lim ? x[c] : -INFINITY;
       }
+#pragma unroll
+      for (int c = 0; c < 128; c += 4) {
+        m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
+      }
+      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * p.scale_log2;
       if (j >= 1) {
         tc::mbar_wait(pv_done, (j - 1) & 1);              // O current, P buffer free
         tc::tc_fence_after();
@@ -204,22 +209,25 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         m_used = mx;
       }
       const float mu = m_used == -INFINITY ? 0.f : m_used;
-      float sum = 0.f;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-mu, -mu);
+      float2 s0 = make_float2(0.f, 0.f), s1 = s0;
       uint8_t* prow = sP + r * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 16; ++c8) {                   // 16 chunks of 8 keys (16 B)
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = tc::fast_exp2(x[c8 * 8 + 2 * e] - mu);
-          const float p1 = tc::fast_exp2(x[c8 * 8 + 2 * e + 1] - mu);
-          sum += p0 + p1;
-          pk[e] = tc::pack_bf16(p0, p1);
+          const float2 t = __ffma2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]), sc2, nm2);
+          const float2 pp = make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
+          if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
+          pk[e] = tc::pack_bf16(pp.x, pp.y);
         }
         const int blk = c8 >> 3, cc = c8 & 7;
         uint4* dst = reinterpret_cast<uint4*>(prow + blk * kTileBytes + ((cc ^ (r & 7)) << 4));
         *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
+      const float2 s01 = __fadd2_rn(s0, s1);
+      const float sum = s01.x + s01.y;
       l += sum;
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
@@ -247,7 +255,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                               tc::pack_bf16(o[8 * v + 6] * inv, o[8 * v + 7] * inv));
       }
     }
-    if (store) p.lse2[((long long)b * p.Hq + h) * p.M + qi] = m_used + log2f(l);
+    // pass-2 bias per query row: lse2 - log2(w_r); +inf for rows past m (they weigh nothing)
+    p.qbias[((long long)b * p.Hq + h) * p.Mb + qi] = store ? m_used + log2f(l) - p.log2w[qi] : INFINITY;
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -257,53 +266,84 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   }
 }
 
+// 32 columns of one key row: acc += exp2(S * scale*log2e - b_q), packed f32x2 FMA/FADD,
+// four independent accumulators.  CUT: column c only counts when c >= cut_from (query index
+// >= key index inside the chunk's causal block).
+template <bool CUT>
+__device__ __forceinline__ void score_chunk(const float* x, const float* bq, float2 sc2, int cut_from,
+                                            float2& a0, float2& a1, float2& a2, float2& a3) {
+  const float4* b4 = reinterpret_cast<const float4*>(bq);
+#pragma unroll
+  for (int e = 0; e < 32; e += 4) {
+    const float4 bb = b4[e >> 2];
+    const float2 t0 = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, make_float2(-bb.x, -bb.y));
+    const float2 t1 = __ffma2_rn(make_float2(x[e + 2], x[e + 3]), sc2, make_float2(-bb.z, -bb.w));
+    float2 p0 = make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
+    float2 p1 = make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
+    if (CUT) {
+      p0.x = e + 0 >= cut_from ? p0.x : 0.f;
+      p0.y = e + 1 >= cut_from ? p0.y : 0.f;
+      p1.x = e + 2 >= cut_from ? p1.x : 0.f;
+      p1.y = e + 3 >= cut_from ? p1.y : 0.f;
+    }
+    if ((e & 4) == 0) { a0 = __fadd2_rn(a0, p0); a1 = __fadd2_rn(a1, p1); }
+    else { a2 = __fadd2_rn(a2, p0); a3 = __fadd2_rn(a3, p1); }
+  }
+}
+
+// Pass 2: 12 warps, one CTA per PAIR of 128-key tiles (both tiles resident or both chunk
+// tiles) so every Q tile fetched from L2 serves 256 keys.  warp 0 TMA (the two K tiles once,
+// Q tiles through a 4-stage ring), warp 1 MMA (per item: S^T_w = K_w Q^T for w = 0, 1 into
+// TMEM buffer 2*(i%2)+w), warp 2 TMEM allocator, warps 4-7 / 8-11 math warpgroup w owns key
+// tile w of the pair (thread r = key r = TMEM lane r).  Items are (q-head, q-tile) pairs.
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      TcParams p) {
   constexpr int KB = D / 64;
-  constexpr int kStages = 3;
+  constexpr int kStages = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = smem;                                   // KB blocks (the 128 keys, A operand)
-  uint8_t* sQ = sK + KB * kTileBytes;                   // kStages x KB blocks
-  float* sb = reinterpret_cast<float*>(sQ + kStages * KB * kTileBytes);   // [2][128] bias per query
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + 256);
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sK = smem;                                   // 2 tiles x KB blocks (A operands)
+  uint8_t* sQ = sK + 2 * KB * kTileBytes;               // kStages x KB blocks
+  float* sb = reinterpret_cast<float*>(sQ + kStages * KB * kTileBytes);   // [2 wg][2 buf][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + 512);
   uint64_t* k_full = bars + 0;
-  uint64_t* q_full = bars + 1;       // [3]
-  uint64_t* q_empty = bars + 4;      // [3]
-  uint64_t* s_full = bars + 7;       // [2]
-  uint64_t* s_free = bars + 9;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_full = bars + 1;                 // [4]
+  uint64_t* q_empty = bars + 5;                // [4]
+  uint64_t* s_full = bars + 9;                 // [2]
+  uint64_t* s_free = bars + 11;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
   const int bgi = blockIdx.y;
   const int b = bgi / p.Hkv, gkv = bgi - b * p.Hkv;
   const long long bg = bgi;
-  const bool resident = tile < p.n_res_tiles;
-  int kstart, klen, k0 = 0;
+  // pair -> tiles: resident pairs first, then chunk pairs
+  const int n_res_pairs = (p.n_res_tiles + 1) / 2;
+  const int n_chunk_tiles = (p.m + 127) / 128;
+  const bool resident = (int)blockIdx.x < n_res_pairs;
+  int n_here, first;                                    // number of tiles in this pair, first tile
   if (resident) {
-    const int2 t = p.res_tiles[tile];
-    kstart = t.x; klen = t.y;
+    first = 2 * blockIdx.x;
+    n_here = min(2, p.n_res_tiles - first);
   } else {
-    k0 = (tile - p.n_res_tiles) * 128;
-    kstart = p.S_tot + k0;
-    klen = min(128, p.m - k0);
+    first = 2 * (blockIdx.x - n_res_pairs);             // chunk tile index
+    n_here = min(2, n_chunk_tiles - first);
   }
-  const int nqt = (p.m + 127) / 128;
-  const int qt_begin = resident ? 0 : k0 / 128;
+  const int nqt = n_chunk_tiles;
+  const int qt_begin = resident ? 0 : first;            // q-tiles that can see the first chunk tile
   const int per_head = nqt - qt_begin;
   const int n_items = p.G * per_head;
 
   if (threadIdx.x == 0) {
     tc::mbar_init(k_full, 1);
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(q_full + i, 1); tc::mbar_init(q_empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 4); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 8); }
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_q); tc::tma_prefetch(&tm_k); }
-  if (warp == 2) tc::tmem_alloc<256>(tmem_slot);
+  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -311,9 +351,15 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 
   if (warp == 0) {
     if (tc::elect_one()) {
-      const int krow = (int)(bg * (p.S_tot + p.M) + kstart);
-      tc::mbar_expect_tx(k_full, KB * kTileBytes);
-      for (int kb = 0; kb < KB; ++kb) tc::tma_load_2d(sK + kb * kTileBytes, &tm_k, k_full, kb * 64, krow);
+      tc::mbar_expect_tx(k_full, 2 * KB * kTileBytes);
+      for (int w = 0; w < 2; ++w) {
+        // a missing second tile loads the first again (never read back)
+        const int t = first + min(w, n_here - 1);
+        const int kstart = resident ? p.res_tiles[t].x : p.S_tot + t * 128;
+        const int krow = (int)(bg * (p.S_tot + p.M) + kstart);
+        for (int kb = 0; kb < KB; ++kb)
+          tc::tma_load_2d(sK + (w * KB + kb) * kTileBytes, &tm_k, k_full, kb * 64, krow);
+      }
       for (int i = 0; i < n_items; ++i) {
         const int st = i % kStages, u = i / kStages;
         if (i >= kStages) tc::mbar_wait(q_empty + st, (u - 1) & 1);
@@ -331,67 +377,79 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       const uint32_t aK = tc::smem_u32(sK), aQ = tc::smem_u32(sQ);
       tc::mbar_wait(k_full, 0);
       for (int i = 0; i < n_items; ++i) {
-        const int st = i % kStages, s = i & 1;
+        const int st = i % kStages, sb2 = i & 1;
         tc::mbar_wait(q_full + st, (i / kStages) & 1);
-        if (i >= 2) tc::mbar_wait(s_free + s, ((i >> 1) - 1) & 1);
+        if (i >= 2) tc::mbar_wait(s_free + sb2, ((i >> 1) - 1) & 1);
         tc::tc_fence_after();
         const uint32_t qb = aQ + st * KB * kTileBytes;
+        for (int w = 0; w < n_here; ++w) {
+          const uint32_t kbase = aK + w * KB * kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = tc::desc_kmajor_sw128(aK + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          const uint64_t db = tc::desc_kmajor_sw128(qb + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          tc::mma_bf16_ss(tmem + s * 128, da, db, idesc, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t da = tc::desc_kmajor_sw128(kbase + (kk >> 2) * kTileBytes + (kk & 3) * 32);
+            const uint64_t db = tc::desc_kmajor_sw128(qb + (kk >> 2) * kTileBytes + (kk & 3) * 32);
+            tc::mma_bf16_ss(tmem + (2 * sb2 + w) * 128, da, db, idesc, kk > 0 ? 1u : 0u);
+          }
         }
-        tc::mma_commit(s_full + s);
+        tc::mma_commit(s_full + sb2);
         tc::mma_commit(q_empty + st);
       }
     }
   } else if (warp >= 4) {
-    const int r = threadIdx.x - 128;                      // key row = TMEM lane
+    const int wg = (warp - 4) >> 2;                       // math warpgroup = key tile of the pair
+    const int r = (threadIdx.x - 128) & 127;              // key row = TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const int key_idx = resident ? 0 : k0 + r;            // chunk-relative key index (chunk tiles)
-    float best = 0.f, acc = 0.f;
-    float x[128];
+    const bool active = wg < n_here;
+    const int t = first + wg;
+    int kstart = 0, klen = 0, key_idx = 0;
+    if (active) {
+      if (resident) { kstart = p.res_tiles[t].x; klen = p.res_tiles[t].y; }
+      else { kstart = p.S_tot + t * 128; klen = min(128, p.m - t * 128); key_idx = t * 128 + r; }
+    }
+    float* my_sb = sb + wg * 256;
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    float best = 0.f;
     for (int i = 0; i < n_items; ++i) {
-      const int s = i & 1;
-      const int hh = gkv * p.G + i / per_head;
+      const int sb2 = i & 1;
+      const int head = i / per_head;
       const int q0 = (qt_begin + i % per_head) * 128;
-      {   // bias b_q = lse2_q - log2 w_q (+inf for queries past m)
-        const int q = q0 + r;
-        sb[s * 128 + r] = q < p.m ? p.lse2[((long long)b * p.Hq + hh) * p.M + q] - p.log2w[q] : INFINITY;
-      }
-      tc::named_bar_sync(1, 128);
-      tc::mbar_wait(s_full + s, (i >> 1) & 1);
+      float* bq = my_sb + sb2 * 128;
+      if (active) bq[r] = p.qbias[((long long)b * p.Hq + gkv * p.G + head) * p.Mb + q0 + r];
+      tc::named_bar_sync(1 + wg, 128);
+      tc::mbar_wait(s_full + sb2, (i >> 1) & 1);
       tc::tc_fence_after();
+      if (active) {
+        const uint32_t tbase = tmem + (2 * sb2 + wg) * 128 + lane_off;
+        const bool cut = !resident && q0 < (t + 1) * 128;   // causal cut inside this block
+        float xa[32], xb[32];
+        tc::tmem_ld32(tbase, xa);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tmem + s * 128 + lane_off + c * 32, x + c * 32);
-      tc::tmem_wait_ld();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_free + s);
-      const float* bq = sb + s * 128;
-      if (resident || q0 >= k0 + 128) {                    // no causal cut inside this block
-#pragma unroll
-        for (int c = 0; c < 128; ++c) acc += tc::fast_exp2(fmaf(x[c], p.scale_log2, -bq[c]));
-      } else {
-#pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const float e = tc::fast_exp2(fmaf(x[c], p.scale_log2, -bq[c]));
-          acc += (q0 + c >= key_idx) ? e : 0.f;
+        for (int c = 0; c < 4; ++c) {
+          float* x = (c & 1) ? xb : xa;
+          float* xn = (c & 1) ? xa : xb;
+          tc::tmem_wait_ld();
+          if (c < 3) tc::tmem_ld32(tbase + (c + 1) * 32, xn);   // next chunk in flight
+          if (!cut) score_chunk<false>(x, bq + c * 32, sc2, 0, a0, a1, a2, a3);
+          else score_chunk<true>(x, bq + c * 32, sc2, key_idx - (q0 + c * 32), a0, a1, a2, a3);
         }
       }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(s_free + sb2);
       if ((i + 1) % per_head == 0) {                       // head finished: max over the group
-        best = fmaxf(best, acc);
-        acc = 0.f;
+        const float2 s01 = __fadd2_rn(a0, a1), s23 = __fadd2_rn(a2, a3);
+        best = fmaxf(best, (s01.x + s01.y) + (s23.x + s23.y));
+        a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
       }
     }
-    if (r < klen) p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
+    if (active && r < klen) p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
   }
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<256>(tmem);
+    tc::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -399,9 +457,10 @@ size_t attn_fwd_tc_smem(int d) {
   const int KB = d / 64;
   return 1024 + (size_t)(KB + 2 + 2 * 2 * KB) * kTileBytes + 16 * 8 + 64;
 }
-size_t attn_score_tc_smem(int d) {
+size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
-  return 1024 + (size_t)(KB + 3 * KB) * kTileBytes + 256 * 4 + 16 * 8 + 64;
+  (void)G;
+  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 512 * 4 + 16 * 8 + 64;
 }
 
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -419,14 +478,14 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
 
 void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, int d,
                           cudaStream_t st) {
-  dim3 grid(p.n_res_tiles + (p.m + 127) / 128, p.B * p.Hkv);
-  const size_t smem = attn_score_tc_smem(d);
+  dim3 grid((p.n_res_tiles + 1) / 2 + ((p.m + 127) / 128 + 1) / 2, p.B * p.Hkv);
+  const size_t smem = attn_score_tc_smem(d, p.G);
   if (d == 128) {
     cudaFuncSetAttribute(attn_score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<128><<<grid, 256, smem, st>>>(tq, tk, p);
+    attn_score_tc_kernel<128><<<grid, 384, smem, st>>>(tq, tk, p);
   } else {
     cudaFuncSetAttribute(attn_score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<64><<<grid, 256, smem, st>>>(tq, tk, p);
+    attn_score_tc_kernel<64><<<grid, 384, smem, st>>>(tq, tk, p);
   }
 }
 
