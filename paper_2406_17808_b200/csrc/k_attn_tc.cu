@@ -278,8 +278,10 @@ __device__ __forceinline__ void score_chunk(const float* x, const float* bq, flo
     const float4 bb = b4[e >> 2];
     const float2 t0 = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, make_float2(-bb.x, -bb.y));
     const float2 t1 = __ffma2_rn(make_float2(x[e + 2], x[e + 3]), sc2, make_float2(-bb.z, -bb.w));
-    float2 p0 = make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
-    float2 p1 = make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
+    // 6 of every 16 exp2 pairs on the FMA pipe (degree-4 polynomial), the rest on MUFU
+    const int step = e >> 2;
+    float2 p0 = (step & 3) == 3 ? tc::exp2_poly2<4>(t0) : make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
+    float2 p1 = (step & 1) ? tc::exp2_poly2<4>(t1) : make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
     if (CUT) {
       p0.x = e + 0 >= cut_from ? p0.x : 0.f;
       p0.y = e + 1 >= cut_from ? p0.y : 0.f;
@@ -306,8 +308,8 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;                                   // 2 tiles x KB blocks (A operands)
   uint8_t* sQ = sK + 2 * KB * kTileBytes;               // kStages x KB blocks
-  float* sb = reinterpret_cast<float*>(sQ + kStages * KB * kTileBytes);   // [2 wg][2 buf][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + 512);
+  float* sb = reinterpret_cast<float*>(sQ + kStages * KB * kTileBytes);   // [kStages][128] q bias
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * 128);
   uint64_t* k_full = bars + 0;
   uint64_t* q_full = bars + 1;                 // [4]
   uint64_t* q_empty = bars + 5;                // [4]
@@ -338,7 +340,9 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 
   if (threadIdx.x == 0) {
     tc::mbar_init(k_full, 1);
-    for (int i = 0; i < kStages; ++i) { tc::mbar_init(q_full + i, 1); tc::mbar_init(q_empty + i, 1); }
+    // a Q stage (tile + its 128 query biases) is free once the MMA read the tile (commit) and
+    // the 8 math warps read the biases
+    for (int i = 0; i < kStages; ++i) { tc::mbar_init(q_full + i, 1); tc::mbar_init(q_empty + i, 9); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 8); }
     tc::fence_mbar_init();
   }
@@ -366,9 +370,10 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         const int hh = gkv * p.G + i / per_head;
         const int q0 = (qt_begin + i % per_head) * 128;
         const int qrow = (int)(((long long)b * p.Hq + hh) * p.M + q0);
-        tc::mbar_expect_tx(q_full + st, KB * kTileBytes);
+        tc::mbar_expect_tx(q_full + st, KB * kTileBytes + 512);
         for (int kb = 0; kb < KB; ++kb)
           tc::tma_load_2d(sQ + (st * KB + kb) * kTileBytes, &tm_q, q_full + st, kb * 64, qrow);
+        tc::bulk_load(sb + st * 128, p.qbias + ((long long)b * p.Hq + hh) * p.Mb + q0, 512, q_full + st);
       }
     }
   } else if (warp == 1) {
@@ -406,17 +411,14 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       if (resident) { kstart = p.res_tiles[t].x; klen = p.res_tiles[t].y; }
       else { kstart = p.S_tot + t * 128; klen = min(128, p.m - t * 128); key_idx = t * 128 + r; }
     }
-    float* my_sb = sb + wg * 256;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
     float best = 0.f;
     for (int i = 0; i < n_items; ++i) {
-      const int sb2 = i & 1;
-      const int head = i / per_head;
+      const int sb2 = i & 1, st = i % kStages;
       const int q0 = (qt_begin + i % per_head) * 128;
-      float* bq = my_sb + sb2 * 128;
-      if (active) bq[r] = p.qbias[((long long)b * p.Hq + gkv * p.G + head) * p.Mb + q0 + r];
-      tc::named_bar_sync(1 + wg, 128);
+      const float* bq = sb + st * 128;
+      tc::mbar_wait(q_full + st, (i / kStages) & 1);      // biases of this item have landed
       tc::mbar_wait(s_full + sb2, (i >> 1) & 1);
       tc::tc_fence_after();
       if (active) {
@@ -436,7 +438,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_free + sb2);
+      if (lane == 0) { tc::mbar_arrive(s_free + sb2); tc::mbar_arrive(q_empty + st); }
       if ((i + 1) % per_head == 0) {                       // head finished: max over the group
         const float2 s01 = __fadd2_rn(a0, a1), s23 = __fadd2_rn(a2, a3);
         best = fmaxf(best, (s01.x + s01.y) + (s23.x + s23.y));
@@ -460,7 +462,7 @@ size_t attn_fwd_tc_smem(int d) {
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
   (void)G;
-  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 512 * 4 + 16 * 8 + 64;
+  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + 16 * 8 + 64;
 }
 
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,

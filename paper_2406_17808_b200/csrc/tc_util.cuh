@@ -63,6 +63,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// 1D bulk copy global -> shared (bytes % 16 == 0, 16-B aligned), completion on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -156,6 +163,36 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// exp2 on the FMA pipe (FA4's trick to offload the MUFU): t = n + f with n = round(t),
+// f in [-0.5, 0.5]; 2^f by a minimax polynomial (degree 4: max rel. error 2.6e-6; degree 3:
+// 7.5e-5, coefficients fitted offline); 2^n added into the exponent field.
+// Inputs are clamped at -126 (result <= 2^-125.5, i.e. ~0, and n >= -126 keeps the exponent
+// addition from wrapping below zero when 2^f < 1).
+template <int DEG>
+__device__ __forceinline__ float2 exp2_poly2(float2 t) {
+  t.x = fmaxf(t.x, -126.f);
+  t.y = fmaxf(t.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);      // 1.5 * 2^23
+  const float2 j = __fadd2_rn(t, magic);                         // round(t) in the low mantissa
+  const float2 jf = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(t, make_float2(-jf.x, -jf.y));
+  float2 p;
+  if (DEG == 4) {
+    p = __ffma2_rn(make_float2(0.009569993242621422f, 0.009569993242621422f), f,
+                   make_float2(0.055917542427778244f, 0.055917542427778244f));
+    p = __ffma2_rn(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
+    p = __ffma2_rn(p, f, make_float2(0.6931218504905701f, 0.6931218504905701f));
+    p = __ffma2_rn(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+  } else {
+    p = __ffma2_rn(make_float2(0.05517052486538887f, 0.05517052486538887f), f,
+                   make_float2(0.24260830879211426f, 0.24260830879211426f));
+    p = __ffma2_rn(p, f, make_float2(0.693260908126831f, 0.693260908126831f));
+    p = __ffma2_rn(p, f, make_float2(0.9999282360076904f, 0.9999282360076904f));
+  }
+  const int nx = __float_as_int(j.x) << 23, ny = __float_as_int(j.y) << 23;
+  return make_float2(__int_as_float(__float_as_int(p.x) + nx), __int_as_float(__float_as_int(p.y) + ny));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
