@@ -28,27 +28,31 @@ namespace {
 constexpr int kTileBytes = 128 * 128;          // one 128-row x 64-col bf16 block (16 KB)
 }
 
+// Pass 1.  Shared-memory bandwidth (128 B/clk/SM) is the binding resource of a 128x128 MMA
+// with both operands in SMEM, so Q and P live in TMEM (A operand from TMEM, "TS" MMAs) and
+// only K/V stream through SMEM (3-stage TMA ring).  TMEM columns: S0 [0,128), S1 [128,256),
+// O [256, 256+D), Q [384, 384+D/2); P of tile j (bf16 pairs) overwrites the upper half of S_(j%2).
+// MMA issue order QK(0) QK(1) PV(0) QK(2) PV(1) ...; tcgen05.mma from one thread execute in
+// order, so QK(j+2) overwrites S_(j%2) only after PV(j) has read P(j) from it.
 template <int D>
 __global__ void __launch_bounds__(256, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_vs, const __grid_constant__ CUtensorMap tm_vc,
                    TcParams p) {
   constexpr int KB = D / 64;                   // 64-element K blocks of a row
-  constexpr int kStages = 2;
+  constexpr int kStages = 3;
+  constexpr uint32_t kColO = 256, kColQ = 384;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sQ = smem;                                   // KB blocks
-  uint8_t* sP = sQ + KB * kTileBytes;                   // 2 blocks (128 keys)
-  uint8_t* sK = sP + 2 * kTileBytes;                    // kStages x KB blocks
+  uint8_t* sK = smem;                                   // kStages x KB blocks
   uint8_t* sV = sK + kStages * KB * kTileBytes;         // kStages x KB blocks
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * KB * kTileBytes);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;      // [2]
-  uint64_t* kv_empty = bars + 3;     // [2]
-  uint64_t* s_full = bars + 5;       // [2]
-  uint64_t* s_free = bars + 7;       // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
+  uint64_t* kv_full = bars + 0;      // [3]
+  uint64_t* kv_empty = bars + 3;     // [3]
+  uint64_t* s_full = bars + 6;       // [2]
+  uint64_t* p_full = bars + 8;       // [2]
+  uint64_t* q_full = bars + 10;
+  uint64_t* pv_done = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -60,35 +64,27 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   const int nt = p.n_res_tiles + n_chunk_tiles;
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(kv_full + i, 1); tc::mbar_init(kv_empty + i, 1);
-      tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 4);
-    }
-    tc::mbar_init(p_full, 4);
+    for (int i = 0; i < kStages; ++i) { tc::mbar_init(kv_full + i, 1); tc::mbar_init(kv_empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
+    tc::mbar_init(q_full, 4);
     tc::mbar_init(pv_done, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&tm_q); tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_vs); tc::tma_prefetch(&tm_vc);
+    tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_vs); tc::tma_prefetch(&tm_vc);
   }
   if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem + 0, tmem + 128};
-  const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer: K/V tiles ----------------
     if (tc::elect_one()) {
-      const int qrow = (int)(((long long)b * p.Hq + h) * p.M + q0);
-      tc::mbar_expect_tx(q_full, KB * kTileBytes);
-      for (int kb = 0; kb < KB; ++kb) tc::tma_load_2d(sQ + kb * kTileBytes, &tm_q, q_full, kb * 64, qrow);
       for (int j = 0; j < nt; ++j) {
-        const int s = j & 1, u = j >> 1;
-        if (j >= 2) tc::mbar_wait(kv_empty + s, (u - 1) & 1);
+        const int s = j % kStages, u = j / kStages;
+        if (j >= kStages) tc::mbar_wait(kv_empty + s, (u - 1) & 1);
         int krow, vrow;
         const CUtensorMap* vm;
         if (j < p.n_res_tiles) {
@@ -116,57 +112,73 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     if (tc::elect_one()) {
       constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 128, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, D, 1);
-      const uint32_t aQ = tc::smem_u32(sQ), aP = tc::smem_u32(sP);
       const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV);
-      auto issue_pv = [&](int i) {
-        tc::mbar_wait(p_full, i & 1);
-        tc::tc_fence_after();
-        const uint32_t vbase = aV + (i & 1) * KB * kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {             // 128 keys = 8 x K16
-          const uint64_t da = tc::desc_kmajor_sw128(aP + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          const uint64_t db = tc::desc_mnmajor_sw128(vbase + kk * 2048, kTileBytes);
-          tc::mma_bf16_ss(tO, da, db, idesc_pv, (i > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(pv_done);
-        tc::mma_commit(kv_empty + (i & 1));
-      };
-      tc::mbar_wait(q_full, 0);
-      for (int j = 0; j < nt; ++j) {
-        const int s = j & 1, u = j >> 1;
-        tc::mbar_wait(kv_full + s, u & 1);
-        if (j >= 2) tc::mbar_wait(s_free + s, (u - 1) & 1);
+      auto qk = [&](int j) {
+        const int s = j % kStages;
+        tc::mbar_wait(kv_full + s, (j / kStages) & 1);
         tc::tc_fence_after();
         const uint32_t kbase = aK + s * KB * kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = tc::desc_kmajor_sw128(aQ + (kk >> 2) * kTileBytes + (kk & 3) * 32);
           const uint64_t db = tc::desc_kmajor_sw128(kbase + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          tc::mma_bf16_ss(tS[s], da, db, idesc_qk, kk > 0 ? 1u : 0u);
+          tc::mma_bf16_ts(tmem + (j & 1) * 128, tmem + kColQ + kk * 8, db, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        tc::mma_commit(s_full + s);
-        if (j >= 1) issue_pv(j - 1);
+        tc::mma_commit(s_full + (j & 1));
+      };
+      auto pv = [&](int j) {
+        tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t vbase = aV + (j % kStages) * KB * kTileBytes;
+        const uint32_t pbase = tmem + (j & 1) * 128 + 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {             // 128 keys = 8 x K16
+          const uint64_t db = tc::desc_mnmajor_sw128(vbase + kk * 2048, kTileBytes);
+          tc::mma_bf16_ts(tmem + kColO, pbase + kk * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(kv_empty + (j % kStages));
+        tc::mma_commit(pv_done);
+      };
+      tc::mbar_wait(q_full, 0);
+      tc::tc_fence_after();
+      qk(0);
+      if (nt > 1) qk(1);
+      for (int j = 0; j < nt; ++j) {
+        pv(j);
+        if (j + 2 < nt) qk(j + 2);
       }
-      issue_pv(nt - 1);
     }
   } else if (warp >= 4) {
     // ---------------- softmax warpgroup ----------------
     const int r = threadIdx.x - 128;                      // query row = TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int qi = q0 + r;                                // chunk-relative query index
+    {   // Q row -> TMEM (A operand of every QK^T)
+      const uint4* src = reinterpret_cast<const uint4*>(p.q_rot + (((long long)b * p.Hq + h) * p.M + qi) * D);
+#pragma unroll
+      const bool in_buf = qi < p.M;                       // rows past the scratch capacity: zeros
+      for (int c = 0; c < D / 32; ++c) {                 // 16 columns (32 bf16) per store
+        uint32_t w[16];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint4 u = in_buf ? src[c * 4 + v] : make_uint4(0u, 0u, 0u, 0u);
+          w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
+        }
+        tc::tmem_st16(tmem + kColQ + lane_off + c * 16, w);
+      }
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(q_full);
+    }
     float m_used = -INFINITY, l = 0.f;
     float x[128];
     for (int j = 0; j < nt; ++j) {
-      const int s = j & 1, u = j >> 1;
-      tc::mbar_wait(s_full + s, u & 1);
+      const uint32_t sb = tmem + (j & 1) * 128 + lane_off;
+      tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tS[s] + lane_off + c * 32, x + c * 32);
+      for (int c = 0; c < 4; ++c) tc::tmem_ld32(sb + c * 32, x + c * 32);
       tc::tmem_wait_ld();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_free + s);
-      // mask + scale (log2 domain)
       int lim;                                            // keys [0, lim) of the tile are visible
       if (j < p.n_res_tiles) {
         lim = p.res_tiles[j].y;
@@ -185,54 +197,51 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
       }
       const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * p.scale_log2;
-      if (j >= 1) {
-        tc::mbar_wait(pv_done, (j - 1) & 1);              // O current, P buffer free
-        tc::tc_fence_after();
+      if (j == 0) {
+        m_used = mx;
+      } else {
         // Lazy rescale of the O row when its max grew by more than 2^8.  tcgen05.ld/st are
-        // warp-collective (.sync.aligned), so the whole warp takes the branch if any row needs it.
+        // warp-collective, so the whole warp takes the branch if any row needs it; O must
+        // hold every PV up to tile j-1 first.
         const bool need = mx > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
+          tc::mbar_wait(pv_done, (j - 1) & 1);
+          tc::tc_fence_after();
           const float f = need ? tc::fast_exp2(m_used - mx) : 1.f;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
-            tc::tmem_ld32(tO + lane_off + c * 32, o);
+            tc::tmem_ld32(tmem + kColO + lane_off + c * 32, o);
             tc::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] *= f;
-            tc::tmem_st32(tO + lane_off + c * 32, o);
+            tc::tmem_st32(tmem + kColO + lane_off + c * 32, o);
           }
-          tc::tmem_wait_st();
           if (need) { l *= f; m_used = mx; }
         }
-      } else {
-        m_used = mx;
       }
       const float mu = m_used == -INFINITY ? 0.f : m_used;
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-mu, -mu);
       float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-      uint8_t* prow = sP + r * 128;
 #pragma unroll
-      for (int c8 = 0; c8 < 16; ++c8) {                   // 16 chunks of 8 keys (16 B)
-        uint32_t pk[4];
+      for (int c = 0; c < 4; ++c) {                       // 32 keys -> 16 packed columns per store
+        uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 t = __ffma2_rn(make_float2(x[c8 * 8 + 2 * e], x[c8 * 8 + 2 * e + 1]), sc2, nm2);
-          const float2 pp = make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
+        for (int e = 0; e < 16; ++e) {
+          const float2 t = __ffma2_rn(make_float2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sc2, nm2);
+          // one pair in four on the FMA pipe (degree-3 polynomial; P is rounded to bf16 anyway)
+          const float2 pp = (e & 3) == 3 ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
           if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
           pk[e] = tc::pack_bf16(pp.x, pp.y);
         }
-        const int blk = c8 >> 3, cc = c8 & 7;
-        uint4* dst = reinterpret_cast<uint4*>(prow + blk * kTileBytes + ((cc ^ (r & 7)) << 4));
-        *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        tc::tmem_st16(sb + 64 + c * 16, pk);
       }
       const float2 s01 = __fadd2_rn(s0, s1);
-      const float sum = s01.x + s01.y;
-      l += sum;
-      tc::fence_proxy_async_smem();
+      l += s01.x + s01.y;
+      tc::tmem_wait_st();
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
+      if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
     }
     // epilogue
     tc::mbar_wait(pv_done, (nt - 1) & 1);
@@ -243,7 +252,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       float o[32];
-      tc::tmem_ld32(tO + lane_off + c * 32, o);
+      tc::tmem_ld32(tmem + kColO + lane_off + c * 32, o);
       tc::tmem_wait_ld();
       if (store) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -457,7 +466,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 
 size_t attn_fwd_tc_smem(int d) {
   const int KB = d / 64;
-  return 1024 + (size_t)(KB + 2 + 2 * 2 * KB) * kTileBytes + 16 * 8 + 64;
+  return 1024 + (size_t)(2 * 3 * KB) * kTileBytes + 16 * 8 + 64;
 }
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
