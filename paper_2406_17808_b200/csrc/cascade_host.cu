@@ -457,7 +457,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     tp.Mb = (g.ldc + 127) / 128 * 128;
     tp.scale_log2 = g.scale_log2;
     tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
-    tp.q_rot = q_rot; tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
+    tp.q_rot = q_rot; tp.k_rot = k_rot; tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);

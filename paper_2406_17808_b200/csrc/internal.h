@@ -97,6 +97,7 @@ struct TcParams {
   int32_t n_res_tiles;
   const int2* res_tiles;        // (start slot, valid length) of each resident key tile
   const __nv_bfloat16* q_rot;   // [B][Hq][M][D]  rotated chunk queries
+  const __nv_bfloat16* k_rot;   // [B][Hkv][S_tot + M][D]  rotated keys (slot order + chunk)
   __nv_bfloat16* out;           // [B][m][Hq][D]
   float* qbias;                 // [B][Hq][Mb] lse2 - log2(w_r): log2-domain LSE of scale*log2e*S
                                 //             minus the EMA row weight (+inf past m)

@@ -1,77 +1,133 @@
 // k_prep.cu -- RoPE by cache rank + layout prep for the attention passes.
 //
 // Writes, for one layer and one chunk:
-//   q_rot  [B][Hq][ldc][d]        chunk queries rotated to pe = n_cached + r
-//   k_rot  [B][Hkv][S_tot + ldc][d] resident keys (flat slot order) rotated to their
-//                                 pre-chunk rank pe (closed form, slot_pe), and chunk
-//                                 keys at rows S_tot + r rotated to n_cached + r
-//   v_chunk[B][Hkv][ldc][d]       chunk values, head-major
-// Keys are cached pre-RoPE (Q11) because ranks change every chunk.  cos/sin come
-// from a table built on the host in float64 and rounded to fp32 (rope_tab[pos][i]).
-// HBM-bound elementwise work: one thread per rotate-half pair, coalesced along d.
+//   q_rot  [B][Hq][ldc][d]          chunk queries rotated to pe = n_cached + r
+//   k_rot  [B][Hkv][S_tot + ldc][d] resident keys (flat slot order) rotated to their pre-chunk
+//                                   rank pe (closed form, slot_pe), chunk keys at rows S_tot + r
+//                                   rotated to n_cached + r
+//   v_chunk[B][Hkv][ldc][d]         chunk values, head-major
+// Keys are cached pre-RoPE (Q11) because ranks change every chunk.  cos/sin come from a table
+// built on the host in float64 and rounded to fp32 (rope_tab[pos][i]).
+//
+// HBM-bound: every thread moves one 16-byte vector of the first half of a row and the
+// matching vector of the second half (rotate-half pairs (i, i + d/2)), so D/(2*EPV) threads
+// cover a row (8 for bf16 d = 128) with fully coalesced 16-byte loads and stores.
 #include "common.cuh"
 
 namespace cascade {
 
+namespace {
+
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void unpack(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y); f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+  __device__ static uint4 pack(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void unpack(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  __device__ static uint4 pack(const float* f) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+// rotate-half on one vector pair: lo = x[i..i+N), hi = x[i+d/2 .. i+d/2+N) at frequencies i..i+N
 template <typename T>
-__global__ void rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* __restrict__ k,
-                                 const T* __restrict__ v, const T* __restrict__ k_raw,
-                                 const float2* __restrict__ tab, T* __restrict__ q_rot,
-                                 T* __restrict__ k_rot, T* __restrict__ v_chunk) {
+__device__ __forceinline__ void rotate(uint4& lo, uint4& hi, const float2* __restrict__ cs) {
+  constexpr int N = Vec<T>::N;
+  float a[N], b[N];
+  Vec<T>::unpack(lo, a);
+  Vec<T>::unpack(hi, b);
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const float2 c = cs[e];
+    const float x1 = a[e], x2 = b[e];
+    a[e] = x1 * c.x - x2 * c.y;
+    b[e] = x2 * c.x + x1 * c.y;
+  }
+  lo = Vec<T>::pack(a);
+  hi = Vec<T>::pack(b);
+}
+
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* __restrict__ k,
+                                                        const T* __restrict__ v, const T* __restrict__ k_raw,
+                                                        const float2* __restrict__ tab, T* __restrict__ q_rot,
+                                                        T* __restrict__ k_rot, T* __restrict__ v_chunk) {
+  constexpr int N = Vec<T>::N;                 // elements per 16-byte vector
   const int half = g.d >> 1;
-  const long long rows_q = (long long)g.B * g.Hq * g.m;
+  const int tpr = half / N;                    // threads per row
+  const long long rows_q = (long long)g.B * g.m * g.Hq;
   const long long rows_k = (long long)g.B * g.Hkv * (g.S_tot + g.m);
-  const long long rows_v = (long long)g.B * g.Hkv * g.m;
-  const long long total = (rows_q + rows_k + rows_v) * half;
+  const long long rows_v = (long long)g.B * g.m * g.Hkv;
+  const long long total = (rows_q + rows_k + rows_v) * tpr;
   for (long long task = blockIdx.x * (long long)blockDim.x + threadIdx.x; task < total;
        task += (long long)gridDim.x * blockDim.x) {
-    long long row = task / half;
-    int i = (int)(task - row * half);
-    if (row < rows_q) {                       // q_rot[b][h][r] <- rope(q[b][r][h], n_c + r)
-      int r = (int)(row % g.m);
-      long long bh = row / g.m;
-      int h = (int)(bh % g.Hq), b = (int)(bh / g.Hq);
-      const T* src = q + (((long long)b * g.m + r) * g.Hq + h) * g.d;
-      float2 cs = tab[(long long)(g.n_cached + r) * half + i];
-      float x1 = to_f(src[i]), x2 = to_f(src[i + half]);
-      T* dst = q_rot + (bh * g.ldc + r) * g.d;
-      dst[i] = from_f<T>(x1 * cs.x - x2 * cs.y);
-      dst[i + half] = from_f<T>(x2 * cs.x + x1 * cs.y);
+    long long row = task / tpr;
+    const int t = (int)(task - row * tpr);
+    const int i0 = t * N;                      // first frequency index of this thread
+    if (row < rows_q) {                        // source order (b, r, h): contiguous reads
+      const int h = (int)(row % g.Hq);
+      const long long br = row / g.Hq;
+      const int r = (int)(br % g.m), b = (int)(br / g.m);
+      const uint4* src = reinterpret_cast<const uint4*>(q + row * g.d);
+      uint4 lo = src[t], hi = src[t + tpr];
+      rotate<T>(lo, hi, tab + (long long)(g.n_cached + r) * half + i0);
+      uint4* dst = reinterpret_cast<uint4*>(q_rot + (((long long)b * g.Hq + h) * g.ldc + r) * g.d);
+      dst[t] = lo; dst[t + tpr] = hi;
       continue;
     }
     row -= rows_q;
     if (row < rows_k) {
       const int ld = g.S_tot + g.m;
-      int x = (int)(row % ld);
-      long long bg = row / ld;
-      const T* src;
+      const int x = (int)(row % ld);
+      const long long bg = row / ld;
+      const uint4* src;
       int pe;
       if (x < g.S_tot) {
         pe = slot_pe(g, x);
-        if (pe < 0) continue;                 // empty slot: never read
-        src = k_raw + (bg * g.S_tot + x) * g.d;
+        if (pe < 0) continue;                  // empty slot: never read
+        src = reinterpret_cast<const uint4*>(k_raw + (bg * g.S_tot + x) * g.d);
       } else {
-        int r = x - g.S_tot;
-        int gg = (int)(bg % g.Hkv), b = (int)(bg / g.Hkv);
+        const int r = x - g.S_tot;
+        const int gg = (int)(bg % g.Hkv), b = (int)(bg / g.Hkv);
         pe = g.n_cached + r;
-        src = k + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
+        src = reinterpret_cast<const uint4*>(k + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
       }
-      float2 cs = tab[(long long)pe * half + i];
-      float x1 = to_f(src[i]), x2 = to_f(src[i + half]);
-      T* dst = k_rot + (bg * (g.S_tot + g.ldc) + x) * g.d;
-      dst[i] = from_f<T>(x1 * cs.x - x2 * cs.y);
-      dst[i + half] = from_f<T>(x2 * cs.x + x1 * cs.y);
+      uint4 lo = src[t], hi = src[t + tpr];
+      rotate<T>(lo, hi, tab + (long long)pe * half + i0);
+      uint4* dst = reinterpret_cast<uint4*>(k_rot + (bg * (g.S_tot + g.ldc) + x) * g.d);
+      dst[t] = lo; dst[t + tpr] = hi;
       continue;
     }
-    row -= rows_k;                            // v_chunk[b][g][r] <- v[b][r][g]
+    row -= rows_k;                             // v_chunk[b][g][r] <- v[b][r][g]
     {
-      int r = (int)(row % g.m);
-      long long bg = row / g.m;
-      int gg = (int)(bg % g.Hkv), b = (int)(bg / g.Hkv);
-      const T* src = v + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-      T* dst = v_chunk + (bg * g.ldc + r) * g.d;
-      dst[i] = src[i];
-      dst[i + half] = src[i + half];
+      const int gg = (int)(row % g.Hkv);
+      const long long br = row / g.Hkv;
+      const int r = (int)(br % g.m), b = (int)(br / g.m);
+      const uint4* src = reinterpret_cast<const uint4*>(v + row * g.d);
+      uint4* dst = reinterpret_cast<uint4*>(v_chunk + (((long long)b * g.Hkv + gg) * g.ldc + r) * g.d);
+      dst[t] = src[t]; dst[t + tpr] = src[t + tpr];
     }
   }
 }
@@ -79,9 +135,10 @@ __global__ void rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* _
 template <typename T>
 void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, const T* k_raw_state,
                       const float2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st) {
-  long long total = ((long long)g.B * g.Hq * g.m + (long long)g.B * g.Hkv * (g.S_tot + g.m) +
-                     (long long)g.B * g.Hkv * g.m) * (g.d / 2);
-  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  const int tpr = (g.d / 2) / Vec<T>::N;
+  const long long total = ((long long)g.B * g.Hq * g.m + (long long)g.B * g.Hkv * (g.S_tot + g.m) +
+                           (long long)g.B * g.Hkv * g.m) * tpr;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
   rope_prep_kernel<T><<<blocks, 256, 0, st>>>(g, q, k, v, k_raw_state, rope_tab, q_rot, k_rot, v_chunk);
 }
 
