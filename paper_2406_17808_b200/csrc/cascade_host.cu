@@ -31,6 +31,7 @@ struct LayerBufs {
   // per-call scratch (per layer so layers may run on different streams)
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
+  float* dec_logits; float* dec_part_o; float* dec_part_ml;
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
 };
 
@@ -66,8 +67,10 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 
 struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
+  size_t dec_logits, dec_part_o, dec_part_ml;
+  int32_t dec_nsplit;
   size_t per_layer;
-  size_t rope_tab, stage_q, stage_kv, stage_out;
+  size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
   size_t total;
   int32_t plan_ints;
 };
@@ -87,19 +90,35 @@ Sizes compute_sizes(const cascade_config& c) {
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
-  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 2 * (S / 128 + N + 2) + 16);
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 2 * (S / 128 + N + 2) + (N + 3) + 16);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
   z.k_rot = align_up(B * Hk * (S + M) * d * es);
   z.v_chunk = align_up(B * Hk * M * d * es);
+  // decode scratch (bf16 only): logits per (slot, q-head of the group) and split partials
+  const size_t G = Hq / Hk;
+  z.dec_nsplit = 0;
+  z.dec_logits = z.dec_part_o = z.dec_part_ml = 0;
+  if (c.dtype == CASCADE_BF16) {
+    const size_t bgs = B * Hk;
+    size_t ns = (148 * 2 * 4 + bgs - 1) / bgs;
+    ns = std::max<size_t>(1, std::min<size_t>(ns, (S + 1 + 511) / 512));
+    z.dec_nsplit = (int32_t)ns;
+    z.dec_logits = align_up(bgs * (S + 1) * G * 4);
+    z.dec_part_o = align_up(bgs * ns * G * d * 4);
+    z.dec_part_ml = align_up(bgs * ns * G * 2 * 4);
+  }
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk;
+                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
+  z.tab_hi = align_up(((S + M) / 64 + 1) * (d / 2) * sizeof(float2));
+  z.tab_lo = align_up(64 * (d / 2) * sizeof(float2));
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
-  z.total = z.per_layer * c.num_layers + z.rope_tab + z.stage_q + 2 * z.stage_kv + z.stage_out;
+  z.total = z.per_layer * c.num_layers + z.rope_tab + z.tab_hi + z.tab_lo + z.stage_q + 2 * z.stage_kv +
+            z.stage_out;
   return z;
 }
 
@@ -114,6 +133,8 @@ struct cascade_handle {
   std::vector<cascade_mirror> mirrors;
   std::vector<int32_t> m_last;
   float2* rope_tab;
+  float2* tab_hi;
+  float2* tab_lo;
   void *stage_q, *stage_k, *stage_v, *stage_out;
   Planner planner;
   Plan plan;
@@ -265,8 +286,13 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.plan = reinterpret_cast<int32_t*>(take(sz.plan));
     L.resolved = reinterpret_cast<int32_t*>(take(sz.resolved));
     L.q_rot = take(sz.q_rot); L.k_rot = take(sz.k_rot); L.v_chunk = take(sz.v_chunk);
+    L.dec_logits = reinterpret_cast<float*>(take(sz.dec_logits));
+    L.dec_part_o = reinterpret_cast<float*>(take(sz.dec_part_o));
+    L.dec_part_ml = reinterpret_cast<float*>(take(sz.dec_part_ml));
   }
   h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
+  h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
+  h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
   h->stage_q = take(sz.stage_q); h->stage_k = take(sz.stage_kv);
   h->stage_v = take(sz.stage_kv); h->stage_out = take(sz.stage_out);
   h->mirrors.assign(cfg->num_layers, cascade_mirror{});
@@ -313,6 +339,18 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     }
     ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(float2),
                           cudaMemcpyHostToDevice) == cudaSuccess;
+    // angle-addition factors for decode: pe = 64 a + b, cos/sin(64 a theta_i) and cos/sin(b theta_i)
+    const size_t nhi = npos / 64 + 1;
+    std::vector<float2> hi(nhi * half), lo(64 * half);
+    for (int i = 0; i < half; ++i) {
+      const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
+      for (size_t a = 0; a < nhi; ++a)
+        hi[a * half + i] = make_float2((float)std::cos(64.0 * a * f), (float)std::sin(64.0 * a * f));
+      for (int bb = 0; bb < 64; ++bb)
+        lo[bb * half + i] = make_float2((float)std::cos(bb * f), (float)std::sin(bb * f));
+    }
+    ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->tab_lo, lo.data(), lo.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
   }
   ok = ok && cudaDeviceSynchronize() == cudaSuccess;
   if (!ok) { cascade_destroy(h); return CASCADE_ERR_CUDA; }
@@ -351,6 +389,7 @@ struct Upload {
   const float* log2w;    // [m] their log2 (-inf when w == 0)
   const int2* tiles;     // resident key tiles (start slot, valid length)
   int32_t n_tiles;
+  const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
 };
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
@@ -388,7 +427,9 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   };
   add_run(0, pre.sink_count);
   for (int32_t i = 0; i < h->N; ++i) add_run(h->alpha + i * h->c, pre.counts[i]);
-  const size_t total = nsel + nord + nmov + 2 * (size_t)m + 2 * (size_t)nt;
+  int32_t* phases = tiles + 2 * nt;
+  for (size_t i = 0; i < P.phase_begin.size(); ++i) phases[i] = P.phase_begin[i];
+  const size_t total = nsel + nord + nmov + 2 * (size_t)m + 2 * (size_t)nt + P.phase_begin.size();
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -402,6 +443,7 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->log2w = up->w + m;
   up->tiles = reinterpret_cast<const int2*>(up->log2w + m);
   up->n_tiles = nt;
+  up->phase_begin = reinterpret_cast<const int32_t*>(up->tiles + nt);
   return CASCADE_OK;
 }
 
@@ -540,7 +582,52 @@ cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, con
 cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,
                               const void* v, void* out, void* stream) {
   // q [B,Hq,d] is [B,1,Hq,d]: the m = 1 case of the strided step (Eq. 2).
-  return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
+  // the fp32 toy and d = 64 run the m = 1 case of the strided kernels; bf16 d = 128 (the
+  // Llama shapes) has the dedicated HBM-oriented decode kernels
+  if (h == nullptr || h->cfg.dtype != CASCADE_BF16 || h->cfg.head_dim != 128)
+    return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
+  cascade_status rc = check_call(h, layer, 1);
+  if (rc != CASCADE_OK) return rc;
+  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerBufs& L = h->layers[layer];
+  const Geometry g = make_geometry(h, h->mirrors[layer], 1);
+  Upload up;
+  cascade_mirror next;
+  rc = upload_plan(h, layer, 1, st, &up, &next);
+  if (rc != CASCADE_OK) return rc;
+  DecodeParams dp{};
+  dp.B = g.B; dp.Hq = g.Hq; dp.Hkv = g.Hkv; dp.G = g.G; dp.S_tot = g.S_tot; dp.alpha = g.alpha;
+  dp.N = g.N; dp.c = g.c; dp.sink_pre = g.sink_pre;
+  for (int i = 0; i < g.N; ++i) { dp.counts[i] = g.counts_pre[i]; dp.xi[i] = g.xi_pre[i]; dp.base[i] = g.base_pre[i]; }
+  dp.n_keys = g.n_cached + 1;
+  dp.t0 = g.t0;
+  dp.scale_log2 = g.scale_log2;
+  dp.w0 = (float)((1.0 - h->cfg.ema_gamma) * gamma_pow(h->cfg.ema_gamma, 0));
+  dp.decay = g.decay;
+  dp.q = static_cast<const __nv_bfloat16*>(q);
+  dp.k_new = static_cast<const __nv_bfloat16*>(k);
+  dp.v_new = static_cast<const __nv_bfloat16*>(v);
+  dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
+  dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
+  dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
+  dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
+  dp.logits = L.dec_logits; dp.part_o = L.dec_part_o; dp.part_ml = L.dec_part_ml;
+  dp.lse2 = L.lse;
+  dp.nsplit = std::min<int32_t>((int32_t)decode_attn_nsplit(dp), h->sz.dec_nsplit);
+  const Plan& P = h->plan;
+  {
+    ProfScope ps(h, 4, st);
+    launch_decode(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin, (int32_t)P.phase_begin.size() - 1,
+                  static_cast<__nv_bfloat16*>(out), g.d, st);
+    // algorithmic bytes: K, V (2 d bf16) + logits (4 G) + mu r/w + s per key
+    ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 4.0 * g.G + 16.0 + 4.0));
+  }
+  h->launches += 3;
+  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  h->mirrors[layer] = next;
+  h->m_last[layer] = 1;
+  return CASCADE_OK;
 }
 
 cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, const void* k,

@@ -104,6 +104,37 @@ struct TcParams {
   const float* log2w;           // [m]  log2 of the EMA row weights
   float* s;                     // [B*Hkv][S_tot + m]
 };
+// single-token decode (k_decode.cu)
+struct DecodeParams {
+  int32_t B, Hq, Hkv, G, S_tot, alpha, N, c;
+  int32_t sink_pre;
+  int32_t counts[CASCADE_MAX_LEVELS], xi[CASCADE_MAX_LEVELS], base[CASCADE_MAX_LEVELS];
+  int32_t n_keys;               // n_cached + 1 (the new token)
+  int32_t nsplit;
+  int64_t t0;                   // stream index of the new token
+  float scale_log2;             // softmax scale * log2(e)
+  float w0;                     // (1 - gamma): EMA weight of the single row (Alg. 3, m = 1)
+  double decay;                 // gamma
+  const __nv_bfloat16* q;       // [B][Hq][D]   pre-RoPE
+  const __nv_bfloat16* k_new;   // [B][Hkv][D]
+  const __nv_bfloat16* v_new;   // [B][Hkv][D]
+  __nv_bfloat16* k_raw_mut;     // state [B*Hkv][S_tot][D]
+  __nv_bfloat16* v_mut;         // state
+  double* mu;                   // state
+  int64_t* origin;              // state
+  float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
+  const float2* tab;            // [npos][D/2] cos/sin(pe theta_i)
+  const float2* tab_hi;         // [npos/64 + 1][D/2] cos/sin(64 a theta_i)
+  const float2* tab_lo;         // [64][D/2] cos/sin(b theta_i)
+  float* logits;                // [B*Hkv][S_tot + 1][G] log2-domain scaled logits
+  float* part_o;                // [B*Hkv][nsplit][G][D]
+  float* part_ml;               // [B*Hkv][nsplit][G][2]
+  float* lse2;                  // [B*Hq]
+};
+size_t decode_attn_nsplit(const DecodeParams& p);
+void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
+                   int32_t n_phase, __nv_bfloat16* out, int d, cudaStream_t st);
+
 size_t attn_fwd_tc_smem(int d);
 size_t attn_score_tc_smem(int d, int G);
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
