@@ -255,6 +255,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2406_17808_b200 import cascade as C
+    from paper_2406_17808_b200.dist import gather_heads, shard_range
     from paper_2406_17808_b200.synth import Synth, config_seed, passkey_depth
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -266,8 +267,8 @@ def main():
     peaks = load_peaks()
 
     Hq, Hk, d = spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"]
-    assert Hk % world == 0, "kv-heads must divide across ranks"
-    hq, hk = Hq // world, Hk // world
+    q_sl, k_sl = shard_range(rank, world, Hq, Hk)          # kv-head sharding (independent heads)
+    hq, hk = q_sl.stop - q_sl.start, k_sl.stop - k_sl.start
     m, T, B = spec["stride"], spec["tokens"], spec["batch"]
     nchunks = (T + m - 1) // m
     cfg = C.CascadeConfig(batch=B, num_q_heads=hq, num_kv_heads=hk, head_dim=d,
@@ -285,9 +286,9 @@ def main():
     V = torch.empty_like(K)
     for c in range(nchunks):
         q, k, v = syn.chunk(c * m, m, device="cuda")
-        Q[c].copy_(q[:, :, rank * hq:(rank + 1) * hq])
-        K[c].copy_(k[:, :, rank * hk:(rank + 1) * hk])
-        V[c].copy_(v[:, :, rank * hk:(rank + 1) * hk])
+        Q[c].copy_(q[:, :, q_sl])
+        K[c].copy_(k[:, :, k_sl])
+        V[c].copy_(v[:, :, k_sl])
     log(f"inputs ready: {nchunks} chunks of {m}")
     O = torch.empty_like(Q)
     O_full = torch.empty((nchunks, world, B, m, hq, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
@@ -304,7 +305,7 @@ def main():
                 ev.record(main_stream)
                 comm.wait_event(ev)
                 with torch.cuda.stream(comm):
-                    dist.all_gather_into_tensor(O_full[c].view(-1), O[c].view(-1))
+                    gather_heads(O[c], world, buf=O_full[c])
         if world > 1:
             main_stream.wait_stream(comm)
 
