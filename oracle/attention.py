@@ -84,6 +84,17 @@ def chunk_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, n_cached: int,
     return P @ v, P
 
 
+def slice_rows(q_rows: np.ndarray, rows: np.ndarray, k: np.ndarray, v: np.ndarray, n_cached: int,
+               scale: float):
+    """Rows `rows` of the same rectangular slice as ``chunk_attention`` (query r sees keys
+    j <= n_cached + r), evaluated for a subset of rows only -- so a long chunk can be checked
+    block by block.  Returns (O [len(rows), d], P [len(rows), n_keys])."""
+    logits = (q_rows @ k.T) * scale
+    visible = np.arange(k.shape[0])[None, :] <= n_cached + np.asarray(rows)[:, None]
+    P = softmax_rows(np.where(visible, logits, -np.inf))
+    return P @ v, P
+
+
 def ema_weights(m: int, gamma: float) -> np.ndarray:
     """C_EMA for rows r = 0..m-1: (1 - gamma) * gamma**(m - (r + 1))."""
     k = m - (np.arange(m) + 1)

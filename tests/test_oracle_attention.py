@@ -251,3 +251,16 @@ def test_round_bf16_against_torch_and_exact_values():
     x = np.random.default_rng(9).standard_normal(100000) * 10
     ref = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).double().numpy()
     np.testing.assert_array_equal(round_bf16(x), ref)
+
+
+def test_slice_rows_equals_chunk_attention_rows():
+    from oracle.attention import slice_rows
+    rng = np.random.default_rng(15)
+    n_c, m = 11, 9
+    q = rng.standard_normal((m, 8))
+    k, v = rng.standard_normal((n_c + m, 8)), rng.standard_normal((n_c + m, 8))
+    o, P = chunk_attention(q, k, v, n_c, 0.3)
+    rows = np.array([0, 4, 8])
+    o2, P2 = slice_rows(q[rows], rows, k, v, n_c, 0.3)
+    np.testing.assert_array_equal(P2, P[rows])
+    np.testing.assert_allclose(o2, o[rows], rtol=0, atol=1e-15)
