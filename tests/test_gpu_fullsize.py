@@ -122,3 +122,49 @@ def test_cfg3_sampled_chunks_match_oracle():
                 np.testing.assert_allclose(s_slots, s_ref, rtol=1e-3, atol=1e-30)
                 tot = 1 - cfg.ema_gamma ** m                   # each head's mass sums to 1 - gamma^m
                 assert tot * (1 - 1e-9) <= s_ref.sum() <= G * tot * (1 + 1e-9)
+
+
+def test_cfg4_decode_step_sampled_sequences_match_oracle():
+    """configs[3] launch shape (64 sequences, 16K cascade + 64 sinks, GQA 32/8, d = 128): state
+    from a score-injected prefix, then decode steps; sequences {0, 63} x kv-groups {0, 7} are
+    recomputed by the oracle (Eq. 2 over the exported state, exact mass, EMA fold)."""
+    spec = CONFIGS["cfg4_decode"]
+    B, Hq, Hkv, d = spec["batch"], spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"]
+    cfg = C.CascadeConfig(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d, sink_size=spec["sink_size"],
+                          cache_size=spec["cache_size"], num_cascades=spec["num_cascades"], max_stride=4096,
+                          dtype="bf16", rope_theta=spec["rope_theta"])
+    gpu = C.Cascade(cfg)
+    syn = Synth(B, Hq, Hkv, d, config_seed(4), eps=spec["eps"])
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    T0 = 40960                                                   # > alpha + c * 2^(N-1): cache full
+    for start in range(0, T0, 4096):
+        _, k, v = syn.chunk(start, 4096, device="cuda")
+        gpu.update_with_scores(0, k, v, torch.rand((B, Hkv, cfg.s_tot + 4096), generator=gen, device="cuda") * 1e-4)
+    G = Hq // Hkv
+    scale = 1.0 / np.sqrt(d)
+    for step in range(3):
+        q, k, v = syn.chunk(T0 + step, 1, device="cuda")
+        q1, k1, v1 = q[:, 0].contiguous(), k[:, 0].contiguous(), v[:, 0].contiguous()
+        st = gpu.state(0)
+        mu_before = st["mu"].cpu().numpy()
+        out = gpu.decode(0, q1, k1, v1).cpu()
+        s_gpu = gpu.last_scores(0).cpu().numpy()
+        st_after = gpu.state(0)
+        qc, kc, vc = q.cpu(), k.cpu(), v.cpu()
+        assert st["n_cached"] == cfg.s_tot                       # full cache: n_c = 16448
+        for b in (0, B - 1):
+            for g in (0, Hkv - 1):
+                heads = list(range(g * G, (g + 1) * G))
+                outs, masses, order, n_c = _oracle_chunk(st, b, g, qc, kc, vc, heads, cfg.ema_gamma,
+                                                         cfg.rope_theta, scale)
+                for h in heads:
+                    assert np.abs(_np(out[b, h]) - outs[h][0]).max() <= 2e-2
+                s_ref = reduce_heads(masses, G, "max")[0]
+                s_slots = np.concatenate([s_gpu[b, g, order], s_gpu[b, g, cfg.s_tot:cfg.s_tot + 1]])
+                np.testing.assert_allclose(s_slots, s_ref, rtol=1e-3, atol=1e-30)
+                # EMA fold of the residents that stayed in place: mu' = gamma * mu + s (P:154)
+                org0, org1 = st["origin"][b, g].cpu().numpy(), st_after["origin"][b, g].cpu().numpy()
+                same = order[org1[order] == org0[order]]
+                mu1 = st_after["mu"][b, g].cpu().numpy()
+                ref = cfg.ema_gamma * mu_before[b, g, same] + s_gpu[b, g, same].astype(np.float64)
+                np.testing.assert_allclose(mu1[same], ref, rtol=1e-12)
