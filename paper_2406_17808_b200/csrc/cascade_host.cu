@@ -33,6 +33,7 @@ struct LayerBufs {
   void* q_rot; void* k_rot; void* v_chunk;
   float* dec_logits; float* dec_part_o; float* dec_part_ml;
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
+  CUtensorMap tm_kraw;                    // TMA map of the pre-RoPE key state (decode)
 };
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -90,7 +91,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
-  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 2 * (S / 128 + N + 2) + (N + 3) + 16);
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + N + 2) + (N + 3) + 32);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -102,8 +103,8 @@ Sizes compute_sizes(const cascade_config& c) {
   z.dec_logits = z.dec_part_o = z.dec_part_ml = 0;
   if (c.dtype == CASCADE_BF16) {
     const size_t bgs = B * Hk;
-    size_t ns = (148 * 2 * 4 + bgs - 1) / bgs;
-    ns = std::max<size_t>(1, std::min<size_t>(ns, (S + 1 + 511) / 512));
+    size_t ns = (148 * 7 + bgs - 1) / bgs;
+    ns = std::max<size_t>(1, std::min<size_t>(ns, ((S / 128 + N + 2) + 1 + 3) / 4));
     z.dec_nsplit = (int32_t)ns;
     z.dec_logits = align_up(bgs * (S + 1) * G * 4);
     z.dec_part_o = align_up(bgs * ns * G * d * 4);
@@ -322,7 +323,8 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
       ok = ok && make_map(&L.tm_q, L.q_rot, B * Hq * M, d) &&
            make_map(&L.tm_k, L.k_rot, B * Hk * ((uint64_t)h->S_tot + M), d) &&
            make_map(&L.tm_vs, L.v, B * Hk * (uint64_t)h->S_tot, d) &&
-           make_map(&L.tm_vc, L.v_chunk, B * Hk * M, d);
+           make_map(&L.tm_vc, L.v_chunk, B * Hk * M, d) &&
+           make_map(&L.tm_kraw, L.k_raw, B * Hk * (uint64_t)h->S_tot, d);
     }
   }
   // RoPE table: (cos, sin)(pos * theta^(-2i/d)) computed in double, rounded to fp32 (Q11).
@@ -390,6 +392,7 @@ struct Upload {
   const int2* tiles;     // resident key tiles (start slot, valid length)
   int32_t n_tiles;
   const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
+  const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, wrap index)
 };
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
@@ -416,7 +419,9 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
     lw[r] = wr > 0 ? (float)std::log2(wr) : -INFINITY;
   }
   // resident key tiles: valid runs (sinks, then sub-caches 1..N) cut into 128-slot tiles
-  int32_t* tiles = reinterpret_cast<int32_t*>(lw + m);
+  auto pad4 = [](size_t x) { return (x + 3) & ~size_t(3); };       // int2 / int4 alignment
+  const size_t tiles_off = pad4(nsel + nord + nmov + 2 * (size_t)m);
+  int32_t* tiles = buf + tiles_off;
   int32_t nt = 0;
   auto add_run = [&](int32_t beg, int32_t len) {
     for (int32_t o = 0; o < len; o += 128) {
@@ -427,9 +432,34 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   };
   add_run(0, pre.sink_count);
   for (int32_t i = 0; i < h->N; ++i) add_run(h->alpha + i * h->c, pre.counts[i]);
-  int32_t* phases = tiles + 2 * nt;
+  int32_t* phases = tiles + 2 * nt;                  // (2 nt ints: phases stay 4-aligned + 2 nt)
   for (size_t i = 0; i < P.phase_begin.size(); ++i) phases[i] = P.phase_begin[i];
-  const size_t total = nsel + nord + nmov + 2 * (size_t)m + 2 * (size_t)nt + P.phase_begin.size();
+  // the same tiles with their rank geometry for decode: pe of key j = pe0 + j, minus c for
+  // j >= jw (a full ring's slots before xi come after its oldest)
+  const size_t dt_off = pad4(tiles_off + 2 * (size_t)nt + P.phase_begin.size());
+  int32_t* dt = buf + dt_off;
+  int32_t ndt = 0;
+  auto add_dec = [&](int32_t x0, int32_t len, int32_t pe0, int32_t jw) {
+    dt[4 * ndt] = x0; dt[4 * ndt + 1] = len; dt[4 * ndt + 2] = pe0; dt[4 * ndt + 3] = jw; ++ndt;
+  };
+  for (int32_t o = 0; o < pre.sink_count; o += 128) add_dec(o, std::min(128, pre.sink_count - o), o, 128);
+  {
+    int32_t base = pre.sink_count;
+    int32_t bases[CASCADE_MAX_LEVELS];
+    for (int32_t i = h->N - 1; i >= 0; --i) { bases[i] = base; base += pre.counts[i]; }
+    for (int32_t i = 0; i < h->N; ++i) {
+      const int32_t cnt = pre.counts[i], xi = pre.xi[i], c = h->c;
+      const bool full = cnt == c;
+      for (int32_t s0 = 0; s0 < cnt; s0 += 128) {
+        const int32_t len = std::min(128, cnt - s0);
+        const int32_t x0 = h->alpha + i * c + s0;
+        if (!full) { add_dec(x0, len, bases[i] + s0, 128); continue; }
+        if (s0 >= xi) add_dec(x0, len, bases[i] + s0 - xi, 128);
+        else add_dec(x0, len, bases[i] + s0 - xi + c, (s0 + len > xi) ? xi - s0 : 128);
+      }
+    }
+  }
+  const size_t total = dt_off + 4 * (size_t)ndt;
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -441,9 +471,10 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   pd->sel_cap = h->cfg.max_stride;
   up->w = reinterpret_cast<const float*>(L.plan + nsel + nord + nmov);
   up->log2w = up->w + m;
-  up->tiles = reinterpret_cast<const int2*>(up->log2w + m);
+  up->tiles = reinterpret_cast<const int2*>(L.plan + tiles_off);
   up->n_tiles = nt;
-  up->phase_begin = reinterpret_cast<const int32_t*>(up->tiles + nt);
+  up->phase_begin = L.plan + tiles_off + 2 * nt;
+  up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
   return CASCADE_OK;
 }
 
@@ -614,12 +645,14 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
   dp.logits = L.dec_logits; dp.part_o = L.dec_part_o; dp.part_ml = L.dec_part_ml;
   dp.lse2 = L.lse;
+  dp.n_tiles = up.n_tiles;
+  dp.dec_tiles = up.dec_tiles;
   dp.nsplit = std::min<int32_t>((int32_t)decode_attn_nsplit(dp), h->sz.dec_nsplit);
   const Plan& P = h->plan;
   {
     ProfScope ps(h, 4, st);
     launch_decode(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin, (int32_t)P.phase_begin.size() - 1,
-                  static_cast<__nv_bfloat16*>(out), g.d, st);
+                  static_cast<__nv_bfloat16*>(out), L.tm_kraw, L.tm_vs, st);
     // algorithmic bytes: K, V (2 d bf16) + logits (4 G) + mu r/w + s per key
     ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 4.0 * g.G + 16.0 + 4.0));
   }

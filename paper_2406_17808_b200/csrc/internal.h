@@ -111,6 +111,8 @@ struct DecodeParams {
   int32_t counts[CASCADE_MAX_LEVELS], xi[CASCADE_MAX_LEVELS], base[CASCADE_MAX_LEVELS];
   int32_t n_keys;               // n_cached + 1 (the new token)
   int32_t nsplit;
+  int32_t n_tiles;              // resident key tiles (the new token is one more)
+  const int4* dec_tiles;        // (start slot, length, pe of key 0, wrap index) per tile
   int64_t t0;                   // stream index of the new token
   float scale_log2;             // softmax scale * log2(e)
   float w0;                     // (1 - gamma): EMA weight of the single row (Alg. 3, m = 1)
@@ -133,7 +135,8 @@ struct DecodeParams {
 };
 size_t decode_attn_nsplit(const DecodeParams& p);
 void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                   int32_t n_phase, __nv_bfloat16* out, int d, cudaStream_t st);
+                   int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
+                   cudaStream_t st);
 
 size_t attn_fwd_tc_smem(int d);
 size_t attn_score_tc_smem(int d, int G);

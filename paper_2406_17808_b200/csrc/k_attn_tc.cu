@@ -154,8 +154,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     const int qi = q0 + r;                                // chunk-relative query index
     {   // Q row -> TMEM (A operand of every QK^T)
       const uint4* src = reinterpret_cast<const uint4*>(p.q_rot + (((long long)b * p.Hq + h) * p.M + qi) * D);
-#pragma unroll
       const bool in_buf = qi < p.M;                       // rows past the scratch capacity: zeros
+#pragma unroll
       for (int c = 0; c < D / 32; ++c) {                 // 16 columns (32 bf16) per store
         uint32_t w[16];
 #pragma unroll

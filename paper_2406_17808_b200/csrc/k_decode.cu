@@ -22,91 +22,71 @@
 namespace cascade {
 
 namespace {
-constexpr int kDecThreads = 128;
 
-struct Run { int32_t kstart, slot, len, base_pe, xi, full; };
-
-// Runs of valid keys in key-index order: sinks, C_1 .. C_N (slot order), new token.
-__device__ __forceinline__ int make_runs(const DecodeParams& p, Run* runs) {
-  int n = 0, k = 0;
-  runs[n++] = {k, 0, p.sink_pre, 0, 0, 0};
-  k += p.sink_pre;
-  for (int i = 0; i < p.N; ++i) {
-    runs[n++] = {k, p.alpha + i * p.c, p.counts[i], p.base[i], p.xi[i], p.counts[i] == p.c};
-    k += p.counts[i];
-  }
-  runs[n++] = {k, p.S_tot, 1, p.n_keys - 1, 0, 0};       // the new token (score slot S_tot)
-  return n;
-}
-
-// key index -> (flat slot, pe)
-__device__ __forceinline__ void key_slot(const DecodeParams& p, const Run* runs, int nr, int k, int& slot,
-                                         int& pe) {
-  int r = 0;
-#pragma unroll 1
-  while (r + 1 < nr && k >= runs[r + 1].kstart) ++r;
-  const int s = k - runs[r].kstart;
-  slot = runs[r].slot + s;
-  if (r == 0) pe = s;                                      // sinks
-  else if (r == nr - 1) pe = runs[r].base_pe;              // new token: pe = n_cached
-  else pe = runs[r].base_pe + (runs[r].full ? (s - runs[r].xi + p.c) % p.c : s);
-}
-
-__device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 }  // namespace
 
-// Tensor-core decode attention (D = 128).  One CTA (4 warps) per (b*Hkv, split); per 128-key tile:
-//   1. cp.async: raw keys -> padded rows, values -> the SWIZZLE_128B layout the MMA reads
-//   2. thread t = key t rotates its key to rank pe, rounds to bf16 (Q17), writes the UMMA
-//      K-major tile (SIMT: the only per-key arithmetic left)
-//   3. S^T[128 keys x 16] = K_rot Q^T           (tcgen05, M = 128, N = 16: G heads + zero rows)
-//   4. thread t reads its key's G logits from TMEM, block max per head, P^T (bf16) -> smem
-//   5. O^T[128 d x 16] += V^T P^T               (tcgen05, A = V^T MN-major, M = d)
-// O^T stays in TMEM across tiles; it is rescaled (per head column) only when a head's max grows.
+// Tensor-core decode attention (D = 128), TMA-fed and warp-specialised.  One CTA per
+// (b*Hkv, split); the keys are the host's resident tile list (128-slot runs of one sub-cache,
+// contiguous in memory) plus a 1-key tile for the new token.
+//   warp 0     producer: TMA of the raw K tile and the V tile (SWIZZLE_128B) + the cos/sin rows
+//              of the tile's 64-position blocks (bulk copies) into a 2-stage ring
+//   warp 1     MMA: S^T[128 keys x 16] = K_rot Q^T, then O^T[128 d x 16] += V^T P^T
+//   warp 2     TMEM allocator
+//   warps 4-7  thread t = key t: rotate the raw key IN PLACE to its rank pe (cos/sin of
+//              (64a + b) theta by angle addition: a-rows from the stage, b-rows resident in
+//              shared memory), round to bf16 (reading Q17); then logits, online softmax, P^T.
+// Tile descriptor (int4, host): start slot, length, pe of key 0, wrap index jw (keys j >= jw
+// of a full ring sit before its oldest slot: pe = pe0 + j - c).
+namespace {
+constexpr int kHiRows = 6;                                   // a-rows per tile (<= 3 per pe range)
+constexpr int kLoStride = 64 * 8 + 8;                        // padded bytes per b-row (bank spread)
+}
+
 template <int G>
-__global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_constant__ CUtensorMap tm_k,
+                                                             const __grid_constant__ CUtensorMap tm_v,
+                                                             DecodeParams p) {
   constexpr int D = 128, HALF = 64;
-  constexpr int KROW = D + 8;                               // padded raw-key row (bf16)
+  constexpr int kStageBytes = 65536 + kHiRows * 512;
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
-  uint8_t* sKrot = dsm;                                     // 2 x 16 KB  K-major SW128 [128 keys x 64 d]
-  uint8_t* sV = sKrot + 32768;                              // 2 x 16 KB  [128 keys x 64 d] SW128
-  uint8_t* sQ = sV + 32768;                                 // 2 x 2 KB   [16 rows x 64 d] SW128
-  uint8_t* sP = sQ + 4096;                                  // 2 x 2 KB   [16 heads x 64 keys] SW128
-  __nv_bfloat16* sKraw = reinterpret_cast<__nv_bfloat16*>(sP + 4096);   // [128][KROW]
+  uint8_t* sStage = dsm;                                    // 2 x [K 32 KB | V 32 KB | hi rows 3 KB]
+  uint8_t* sQ = sStage + 2 * kStageBytes;                   // [16 rows x 128 d] SW128 (2 x 2 KB)
+  uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
+  uint8_t* sLo = sP + 4096;                                 // 64 x kLoStride: cos/sin(b theta_i)
   __shared__ float sRed[4][G];
   __shared__ float sCorr[G];
-  __shared__ Run sRuns[CASCADE_MAX_LEVELS + 2];
-  __shared__ int sNr, sRescale;
+  __shared__ int sRescale;
   __shared__ uint32_t sTmem;
-  __shared__ __align__(8) uint64_t bar_s, bar_o;
+  __shared__ __align__(8) uint64_t bars[8];
+  uint64_t* full = bars + 0;        // [2]
+  uint64_t* empty = bars + 2;       // [2]
+  uint64_t* rot_full = bars + 4;
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* pv_done = bars + 7;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bg = blockIdx.x, split = blockIdx.y;            // bg fastest: same pe range per split
+  const int bg = blockIdx.x, split = blockIdx.y;
   const int b = bg / p.Hkv, g = bg - b * p.Hkv;
-  const int per = (p.n_keys + p.nsplit - 1) / p.nsplit;
-  const int kbeg = split * per, kend = min(p.n_keys, kbeg + per);
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const int n_tiles = p.n_tiles + 1;                         // + the new-token tile
+  const int per = (n_tiles + p.nsplit - 1) / p.nsplit;
+  const int tbeg = split * per, tend = min(n_tiles, tbeg + per);
+  const int nt = max(0, tend - tbeg);
 
   if (tid == 0) {
-    sNr = make_runs(p, sRuns);
-    tc::mbar_init(&bar_s, 1);
-    tc::mbar_init(&bar_o, 1);
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
+    tc::mbar_init(rot_full, 4);
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(pv_done, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<32>(&sTmem);
-  // queries of the group rotated to pe = n_cached, rounded to bf16 (rows >= G are zero)
-  for (int o = tid; o < 16 * HALF; o += kDecThreads) {
+  if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_v); }
+  if (warp == 2) tc::tmem_alloc<32>(&sTmem);
+  // group queries rotated to pe = n_cached, bf16 (rows >= G zero); cos/sin(b theta) rows
+  for (int o = tid; o < 16 * HALF; o += blockDim.x) {
     const int h = o / HALF, i = o - h * HALF;
     float r1 = 0.f, r2 = 0.f;
     if (h < G) {
@@ -116,194 +96,262 @@ __global__ void __launch_bounds__(kDecThreads) decode_attn_kernel(DecodeParams p
       r1 = x1 * cs.x - x2 * cs.y;
       r2 = x2 * cs.x + x1 * cs.y;
     }
-    // K-major SW128: row h at h*128 B, 16-B chunk (i/8) XOR (h%8), element i%8
     const int off = h * 128 + ((((i >> 3) ^ (h & 7))) << 4) + (i & 7) * 2;
     *reinterpret_cast<__nv_bfloat16*>(sQ + off) = __float2bfloat16_rn(r1);
     *reinterpret_cast<__nv_bfloat16*>(sQ + 2048 + off) = __float2bfloat16_rn(r2);
   }
-  for (int o = tid; o < 4096 / 16; o += kDecThreads) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
+  for (int o = tid; o < 64 * HALF; o += blockDim.x)
+    *reinterpret_cast<float2*>(sLo + (o / HALF) * kLoStride + (o % HALF) * 8) = p.tab_lo[o];
+  for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = sTmem, tS = tmem, tO = tmem + 16;
-  const int nr = sNr;
 
-  float m_run[G], l_part[G];
-#pragma unroll
-  for (int h = 0; h < G; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
-  const int ntiles = (kend - kbeg + 127) / 128;
-  constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 16, 0, 0);
-  constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, 16, 0, 1);
+  // per-tile geometry (same on every warp): start slot, length, pe0, wrap index
+  auto tile_info = [&](int ti, int& start, int& len, int& pe0, int& jw) {
+    if (ti < p.n_tiles) {
+      const int4 t4 = p.dec_tiles[ti];
+      start = t4.x; len = t4.y; pe0 = t4.z; jw = t4.w;
+    } else {
+      start = p.S_tot; len = 1; pe0 = p.n_keys - 1; jw = 1;     // the new token
+    }
+  };
 
-  for (int t = 0; t < ntiles; ++t) {
-    const int k0 = kbeg + t * 128;
-    if (t > 0) tc::mbar_wait(&bar_o, (t - 1) & 1);          // previous PV has read sV / sP
-    // ---- 1. loads: each warp row-group, lanes over 16-byte chunks (2 rows per instruction) ----
-    for (int rr = warp * 2 + (lane >> 4); rr < 128; rr += 8) {
-      const int ch = lane & 15, k = k0 + rr;
-      uint8_t* vdst = sV + (ch >> 3) * 16384 + rr * 128 + ((((ch & 7) ^ (rr & 7))) << 4);
-      if (k < kend) {
-        int slot, pe;
-        key_slot(p, sRuns, nr, k, slot, pe);
-        const __nv_bfloat16 *ks, *vs;
-        if (slot < p.S_tot) {
-          ks = p.k_raw_mut + ((long long)bg * p.S_tot + slot) * D;
-          vs = p.v_mut + ((long long)bg * p.S_tot + slot) * D;
-        } else {
-          ks = p.k_new + (long long)bg * D;
-          vs = p.v_new + (long long)bg * D;
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      for (int j = 0; j < nt; ++j) {
+        const int s = j & 1;
+        if (j >= 2) tc::mbar_wait(empty + s, ((j >> 1) - 1) & 1);
+        int start, len, pe0, jw;
+        tile_info(tbeg + j, start, len, pe0, jw);
+        uint8_t* st = sStage + s * kStageBytes;
+        // a-rows of the tile's pe ranges: [pe0, pe0+jw) and [pe0+jw-c, pe0+len-c)
+        const int a0 = pe0 >> 6, a1 = (pe0 + min(jw, len) - 1) >> 6;
+        const int nA = a1 - a0 + 1;
+        int nB = 0, b0 = 0;
+        if (jw < len) { b0 = (pe0 + jw - p.c) >> 6; nB = ((pe0 + len - 1 - p.c) >> 6) - b0 + 1; }
+        const uint32_t bytes = (start < p.S_tot ? 65536u : 0u) + (uint32_t)(nA + nB) * 512u;
+        tc::mbar_expect_tx(full + s, bytes);
+        if (start < p.S_tot) {
+          const int row = (int)((long long)bg * p.S_tot + start);
+          for (int kb = 0; kb < 2; ++kb) {
+            tc::tma_load_2d(st + kb * 16384, &tm_k, full + s, kb * 64, row);
+            tc::tma_load_2d(st + 32768 + kb * 16384, &tm_v, full + s, kb * 64, row);
+          }
         }
-        cp_async16(sKraw + rr * KROW + ch * 8, ks + ch * 8);
-        cp_async16(vdst, vs + ch * 8);
-      } else {
-        *reinterpret_cast<uint4*>(sKraw + rr * KROW + ch * 8) = make_uint4(0u, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(vdst) = make_uint4(0u, 0u, 0u, 0u);
+        for (int r = 0; r < nA; ++r) tc::bulk_load(st + 65536 + r * 512, p.tab_hi + (long long)(a0 + r) * HALF, 512, full + s);
+        for (int r = 0; r < nB; ++r) tc::bulk_load(st + 65536 + (3 + r) * 512, p.tab_hi + (long long)(b0 + r) * HALF, 512, full + s);
       }
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    // ---- 2. rotate key t to its rank and write the bf16 K-major tile ----
-    const int k = k0 + tid;
-    const bool valid = k < kend;
-    int slot = 0, pe = 0;
-    if (valid) key_slot(p, sRuns, nr, k, slot, pe);
-    {
-      const __nv_bfloat16* krow = sKraw + tid * KROW;
-      const float4* trow = reinterpret_cast<const float4*>(p.tab + (long long)pe * HALF);
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 16, 0, 0);
+      constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, 16, 0, 1);
+      const uint32_t aQ = tc::smem_u32(sQ), aP = tc::smem_u32(sP);
+      for (int j = 0; j < nt; ++j) {
+        const uint32_t st = tc::smem_u32(sStage + (j & 1) * kStageBytes);
+        tc::mbar_wait(rot_full, j & 1);                       // rotated key tile in place
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t da = tc::desc_kmajor_sw128(st + (kk >> 2) * 16384 + (kk & 3) * 32);
+          const uint64_t db = tc::desc_kmajor_sw128(aQ + (kk >> 2) * 2048 + (kk & 3) * 32);
+          tc::mma_bf16_ss(tS, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(s_full);
+        tc::mbar_wait(p_full, j & 1);                         // P^T written (and O^T rescaled)
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t da = tc::desc_mnmajor_sw128(st + 32768 + kk * 2048, 16384);
+          const uint64_t db = tc::desc_kmajor_sw128(aP + (kk >> 2) * 2048 + (kk & 3) * 32);
+          tc::mma_bf16_ss(tO, da, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(pv_done);
+        tc::mma_commit(empty + (j & 1));
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = tid - 128;                                 // key row of the tile = TMEM lane
+    const int w4 = warp - 4;
+    const uint32_t lane_off = (uint32_t)(w4 * 32) << 16;
+    float m_run[G], l_part[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
+    for (int j = 0; j < nt; ++j) {
+      const int s = j & 1;
+      uint8_t* st = sStage + s * kStageBytes;
+      int start, len, pe0, jw;
+      tile_info(tbeg + j, start, len, pe0, jw);
+      const bool valid = t < len;
+      const int pe = pe0 + t - (t >= jw ? p.c : 0);
+      tc::mbar_wait(full + s, (j >> 1) & 1);
+      if (start < p.S_tot) {
+        // ---- rotate row t in place: pairs (i, i + 64) live at the same swizzled offset of the
+        //      two 64-column blocks ----
+        const int a = pe >> 6;
+        const int hr = t < jw ? a - (pe0 >> 6) : 3 + a - ((pe0 + jw - p.c) >> 6);
+        const float2* hi = reinterpret_cast<const float2*>(st + 65536 + (valid ? hr : 0) * 512);
+        const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 63) * kLoStride);
 #pragma unroll 2
-      for (int c = 0; c < 8; ++c) {                         // 8 pairs (16 bytes of each half) per step
-        const uint4 ua = *reinterpret_cast<const uint4*>(krow + c * 8);
-        const uint4 ub = *reinterpret_cast<const uint4*>(krow + HALF + c * 8);
-        const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w}, wb[4] = {ub.x, ub.y, ub.z, ub.w};
-        uint32_t oa[4], ob[4];
+        for (int c = 0; c < 8; ++c) {
+          const int off = t * 128 + ((c ^ (t & 7)) << 4);
+          uint4* pa = reinterpret_cast<uint4*>(st + off);
+          uint4* pb = reinterpret_cast<uint4*>(st + 16384 + off);
+          const uint4 ua = *pa, ub = *pb;
+          const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w}, wb[4] = {ub.x, ub.y, ub.z, ub.w};
+          uint32_t oa[4], ob[4];
 #pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-          const float4 cs = __ldg(trow + c * 4 + e2);       // (cos, sin) of pairs 2*e2, 2*e2+1
-          const float a0 = __uint_as_float(wa[e2] << 16), a1 = __uint_as_float(wa[e2] & 0xffff0000u);
-          const float b0 = __uint_as_float(wb[e2] << 16), b1 = __uint_as_float(wb[e2] & 0xffff0000u);
-          oa[e2] = tc::pack_bf16(a0 * cs.x - b0 * cs.y, a1 * cs.z - b1 * cs.w);
-          ob[e2] = tc::pack_bf16(b0 * cs.x + a0 * cs.y, b1 * cs.z + a1 * cs.w);
+          for (int e2 = 0; e2 < 4; ++e2) {
+            float r[4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int i = c * 8 + 2 * e2 + u;
+              const float2 h2 = hi[i], l2 = lo[i];
+              const float cs = h2.x * l2.x - h2.y * l2.y;  // cos((64a + b) theta_i)
+              const float sn = h2.y * l2.x + h2.x * l2.y;  // sin((64a + b) theta_i)
+              const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
+              const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
+              r[u] = x1 * cs - x2 * sn;
+              r[2 + u] = x2 * cs + x1 * sn;
+            }
+            oa[e2] = tc::pack_bf16(r[0], r[1]);
+            ob[e2] = tc::pack_bf16(r[2], r[3]);
+          }
+          *pa = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+          *pb = make_uint4(ob[0], ob[1], ob[2], ob[3]);
         }
-        const int sw = ((c ^ (tid & 7)) << 4);
-        *reinterpret_cast<uint4*>(sKrot + tid * 128 + sw) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
-        *reinterpret_cast<uint4*>(sKrot + 16384 + tid * 128 + sw) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+      } else {
+        // ---- the new token: key row 0 from the input, rotated to n_cached; rows >= 1 zero ----
+        const int off_base = t * 128;
+        for (int c = 0; c < 8; ++c) {
+          const int off = off_base + ((c ^ (t & 7)) << 4);
+          uint4 ka = make_uint4(0u, 0u, 0u, 0u), kb2 = ka, va = ka, vb = ka;
+          if (t == 0) {
+            const uint4* kp = reinterpret_cast<const uint4*>(p.k_new + (long long)bg * D);
+            const uint4* vp = reinterpret_cast<const uint4*>(p.v_new + (long long)bg * D);
+            const uint4 ua = kp[c], ub = kp[8 + c];
+            va = vp[c]; vb = vp[8 + c];
+            const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w}, wb[4] = {ub.x, ub.y, ub.z, ub.w};
+            uint32_t oa[4], ob[4];
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              float r[4];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int i = c * 8 + 2 * e2 + u;
+                const float2 cs = p.tab[(long long)pe * HALF + i];
+                const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
+                const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
+                r[u] = x1 * cs.x - x2 * cs.y;
+                r[2 + u] = x2 * cs.x + x1 * cs.y;
+              }
+              oa[e2] = tc::pack_bf16(r[0], r[1]);
+              ob[e2] = tc::pack_bf16(r[2], r[3]);
+            }
+            ka = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            kb2 = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+          }
+          *reinterpret_cast<uint4*>(st + off) = ka;
+          *reinterpret_cast<uint4*>(st + 16384 + off) = kb2;
+          *reinterpret_cast<uint4*>(st + 32768 + off) = va;
+          *reinterpret_cast<uint4*>(st + 49152 + off) = vb;
+        }
       }
-    }
-    tc::fence_proxy_async_smem();
-    __syncthreads();
-    // ---- 3. S^T = K_rot Q^T ----
-    if (tid == 0) {
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(rot_full);
+      // ---- logits, block max per head, P^T ----
+      tc::mbar_wait(s_full, j & 1);
       tc::tc_fence_after();
-      const uint32_t aK = tc::smem_u32(sKrot), aQ = tc::smem_u32(sQ);
+      float sv[16];
+      tc::tmem_ld16(tS + lane_off, sv);
+      tc::tmem_wait_ld();
+      float lg[G];
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint64_t da = tc::desc_kmajor_sw128(aK + (kk >> 2) * 16384 + (kk & 3) * 32);
-        const uint64_t db = tc::desc_kmajor_sw128(aQ + (kk >> 2) * 2048 + (kk & 3) * 32);
-        tc::mma_bf16_ss(tS, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+      for (int h = 0; h < G; ++h) lg[h] = valid ? sv[h] * p.scale_log2 : -INFINITY;
+      if (valid) {
+        float* lp = p.logits + ((long long)bg * (p.S_tot + 1) + start + t) * G;
+#pragma unroll
+        for (int h = 0; h < G; ++h) lp[h] = lg[h];
       }
-      tc::mma_commit(&bar_s);
-    }
-    tc::mbar_wait(&bar_s, t & 1);
-    tc::tc_fence_after();
-    float sv[16];
-    tc::tmem_ld16(tS + lane_off, sv);
-    tc::tmem_wait_ld();
-    // ---- 4. logits, block max per head, P^T ----
-    float lg[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) lg[h] = valid ? sv[h] * p.scale_log2 : -INFINITY;
-    if (valid) {
-      float* lp = p.logits + ((long long)bg * (p.S_tot + 1) + slot) * G;
-#pragma unroll
-      for (int h = 0; h < G; ++h) lp[h] = lg[h];
-    }
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float v = lg[h];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) sRed[warp][h] = v;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int any = 0;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        const float mt = fmaxf(fmaxf(sRed[0][h], sRed[1][h]), fmaxf(sRed[2][h], sRed[3][h]));
-        const float mn = fmaxf(m_run[h], mt);
-        const float cr = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
-        sCorr[h] = cr;
-        any |= (t > 0 && cr != 1.f);
-        sRed[0][h] = mn;                                     // broadcast the new max
+        float v = lg[h];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) sRed[w4][h] = v;
       }
-      sRescale = any;
+      tc::named_bar_sync(1, 128);
+      if (t == 0) {
+        int any = 0;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float mt = fmaxf(fmaxf(sRed[0][h], sRed[1][h]), fmaxf(sRed[2][h], sRed[3][h]));
+          const float mn = fmaxf(m_run[h], mt);
+          const float cr = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+          sCorr[h] = cr;
+          any |= (j > 0 && cr != 1.f);
+          sRed[0][h] = mn;
+        }
+        sRescale = any;
+      }
+      if (j >= 1) tc::mbar_wait(pv_done, (j - 1) & 1);      // sP free, O^T holds tiles < j
+      tc::named_bar_sync(1, 128);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float mn = sRed[0][h];
+        const float cr = sCorr[h];
+        m_run[h] = mn;
+        const float pv = valid ? exp2f(lg[h] - mn) : 0.f;
+        l_part[h] = l_part[h] * cr + pv;
+        const int blk = t >> 6, kc = t & 63;
+        *reinterpret_cast<__nv_bfloat16*>(sP + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
+            __float2bfloat16_rn(pv);
+      }
+      if (sRescale) {                                        // O^T column h *= corr_h (lane = d)
+        float ov[16];
+        tc::tmem_ld16(tO + lane_off, ov);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < G; ++h) ov[h] *= sCorr[h];
+        tc::tmem_st16(tO + lane_off, reinterpret_cast<const uint32_t*>(ov));
+        tc::tmem_wait_st();
+      }
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::named_bar_sync(1, 128);                            // sRed / sCorr reads done
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full);
     }
-    __syncthreads();
+    // ---- split results ----
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      const float mn = sRed[0][h];
-      const float cr = sCorr[h];
-      m_run[h] = mn;
-      const float pv = valid ? exp2f(lg[h] - mn) : 0.f;
-      l_part[h] = l_part[h] * cr + pv;
-      // P^T as the B operand: K-major [16 heads x 128 keys] SW128 (2 blocks of 64 keys)
-      const int blk = tid >> 6, kc = tid & 63;
-      *reinterpret_cast<__nv_bfloat16*>(sP + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
-          __float2bfloat16_rn(pv);
+      float v = l_part[h];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) sRed[w4][h] = v;
     }
-    if (sRescale) {                                          // O^T column h *= corr_h (lane = d)
-      float ov[16];
-      tc::tmem_ld16(tO + lane_off, ov);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int h = 0; h < G; ++h) ov[h] *= sCorr[h];
-      tc::tmem_st16(tO + lane_off, reinterpret_cast<const uint32_t*>(ov));
-      tc::tmem_wait_st();
+    if (nt > 0) tc::mbar_wait(pv_done, (nt - 1) & 1);
+    tc::tc_fence_after();
+    tc::named_bar_sync(1, 128);
+    const long long pbase = ((long long)bg * p.nsplit + split) * G;
+    if (t < G) {
+      p.part_ml[(pbase + t) * 2] = m_run[t];
+      p.part_ml[(pbase + t) * 2 + 1] = sRed[0][t] + sRed[1][t] + sRed[2][t] + sRed[3][t];
     }
-    tc::fence_proxy_async_smem();
-    tc::tc_fence_before();
-    __syncthreads();
-    // ---- 5. O^T += V^T P^T ----
-    if (tid == 0) {
-      tc::tc_fence_after();
-      const uint32_t aV = tc::smem_u32(sV), aP = tc::smem_u32(sP);
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {                      // 128 keys = 8 x K16
-        const uint64_t da = tc::desc_mnmajor_sw128(aV + kk * 2048, 16384);
-        const uint64_t db = tc::desc_kmajor_sw128(aP + (kk >> 2) * 2048 + (kk & 3) * 32);
-        tc::mma_bf16_ss(tO, da, db, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
-      }
-      tc::mma_commit(&bar_o);
-    }
-  }
-  // ---- split results ----
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float v = l_part[h];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) sRed[warp][h] = v;
-  }
-  if (ntiles > 0) tc::mbar_wait(&bar_o, (ntiles - 1) & 1);
-  tc::tc_fence_after();
-  __syncthreads();
-  const long long pbase = ((long long)bg * p.nsplit + split) * G;
-  if (tid < G) {
-    p.part_ml[(pbase + tid) * 2] = m_run[tid];
-    p.part_ml[(pbase + tid) * 2 + 1] = sRed[0][tid] + sRed[1][tid] + sRed[2][tid] + sRed[3][tid];
-  }
-  {
     float ov[16];
     tc::tmem_ld16(tO + lane_off, ov);
     tc::tmem_wait_ld();
 #pragma unroll
-    for (int h = 0; h < G; ++h) p.part_o[(pbase + h) * D + tid] = ntiles > 0 ? ov[h] : 0.f;
+    for (int h = 0; h < G; ++h) p.part_o[(pbase + h) * D + t] = nt > 0 ? ov[h] : 0.f;
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 2) {
     tc::tc_fence_after();
     tc::tmem_dealloc<32>(tmem);
   }
@@ -406,25 +454,25 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
 
 size_t decode_attn_nsplit(const DecodeParams& p) {
   const int bgs = p.B * p.Hkv;
-  int ns = (148 * 2 * 4 + bgs - 1) / bgs;                 // ~4 waves at 2 CTAs / SM
-  ns = std::max(1, std::min(ns, (p.n_keys + 511) / 512)); // >= 512 keys per split
+  int ns = (148 * 7 + bgs - 1) / bgs;                     // ~7 waves at 1 CTA / SM
+  ns = std::max(1, std::min(ns, (p.n_tiles + 1 + 3) / 4)); // >= 4 tiles per split
   return (size_t)ns;
 }
 
 template <int G>
-void launch_attn(const DecodeParams& p, cudaStream_t st) {
-  const size_t smem = 1024 + 32768 + 32768 + 4096 + 4096 + 128 * (128 + 8) * 2;
+void launch_attn(const DecodeParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
+  const size_t smem = 1024 + 2 * (65536 + kHiRows * 512) + 4096 + 4096 + 64 * kLoStride;
   cudaFuncSetAttribute(decode_attn_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  decode_attn_kernel<G><<<dim3(p.B * p.Hkv, p.nsplit), kDecThreads, smem, st>>>(p);
+  decode_attn_kernel<G><<<dim3(p.B * p.Hkv, p.nsplit), 256, smem, st>>>(tk, tv, p);
 }
 
 void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                   int32_t n_phase, __nv_bfloat16* out, int d, cudaStream_t st) {
-  (void)d;   // the caller routes only head_dim 128 here
-  if (p.G == 4) launch_attn<4>(p, st);
-  else if (p.G == 1) launch_attn<1>(p, st);
-  else if (p.G == 2) launch_attn<2>(p, st);
-  else launch_attn<8>(p, st);
+                   int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
+                   cudaStream_t st) {
+  if (p.G == 4) launch_attn<4>(p, tk, tv, st);
+  else if (p.G == 1) launch_attn<1>(p, tk, tv, st);
+  else if (p.G == 2) launch_attn<2>(p, tk, tv, st);
+  else launch_attn<8>(p, tk, tv, st);
   decode_combine_kernel<128><<<p.B * p.Hq, 128, 0, st>>>(p, out);
   decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
 }
