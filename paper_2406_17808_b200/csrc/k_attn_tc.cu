@@ -304,13 +304,15 @@ __device__ __forceinline__ void score_chunk(const float* x, const float* bq, flo
   }
 }
 
-// Pass 2: 12 warps, one CTA per PAIR of 128-key tiles (both tiles resident or both chunk
+// Pass 2: 20 warps, one CTA per PAIR of 128-key tiles (both tiles resident or both chunk
 // tiles) so every Q tile fetched from L2 serves 256 keys.  warp 0 TMA (the two K tiles once,
 // Q tiles through a 4-stage ring), warp 1 MMA (per item: S^T_w = K_w Q^T for w = 0, 1 into
-// TMEM buffer 2*(i%2)+w), warp 2 TMEM allocator, warps 4-7 / 8-11 math warpgroup w owns key
-// tile w of the pair (thread r = key r = TMEM lane r).  Items are (q-head, q-tile) pairs.
+// TMEM buffer 2*(i%2)+w), warp 2 TMEM allocator, warps 4-19 four math warpgroups: warpgroup
+// (half, w) reads key tile w's S^T columns [64 half, 64 half + 64) (thread r = key r = TMEM
+// lane r), so every SMSP has four exp2 warps to hide MUFU/TMEM latency.  Items are
+// (q-head, q-tile); the two column halves meet in shared memory per head before the max.
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(640, 1)
 attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      TcParams p) {
   constexpr int KB = D / 64;
@@ -320,7 +322,8 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   uint8_t* sK = smem;                                   // 2 tiles x KB blocks (A operands)
   uint8_t* sQ = sK + 2 * KB * kTileBytes;               // kStages x KB blocks
   float* sb = reinterpret_cast<float*>(sQ + kStages * KB * kTileBytes);   // [kStages][128] q bias
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * 128);
+  float* sacc = sb + kStages * 128;                     // [2 tiles][2 halves][G][128] partial sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sacc + 4 * p.G * 128);
   uint64_t* k_full = bars + 0;
   uint64_t* q_full = bars + 1;                 // [4]
   uint64_t* q_empty = bars + 5;                // [4]
@@ -353,8 +356,8 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
     tc::mbar_init(k_full, 1);
     // a Q stage (tile + its 128 query biases) is free once the MMA read the tile (commit) and
     // the 8 math warps read the biases
-    for (int i = 0; i < kStages; ++i) { tc::mbar_init(q_full + i, 1); tc::mbar_init(q_empty + i, 9); }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 8); }
+    for (int i = 0; i < kStages; ++i) { tc::mbar_init(q_full + i, 1); tc::mbar_init(q_empty + i, 17); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(s_free + i, 16); }
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_q); tc::tma_prefetch(&tm_k); }
@@ -412,7 +415,8 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       }
     }
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;                       // math warpgroup = key tile of the pair
+    const int wgi = (warp - 4) >> 2;                      // 0..3
+    const int wg = wgi & 1, half = wgi >> 1;              // key tile of the pair, column half
     const int r = (threadIdx.x - 128) & 127;              // key row = TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const bool active = wg < n_here;
@@ -422,27 +426,25 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       if (resident) { kstart = p.res_tiles[t].x; klen = p.res_tiles[t].y; }
       else { kstart = p.S_tot + t * 128; klen = min(128, p.m - t * 128); key_idx = t * 128 + r; }
     }
+    float* my_acc = sacc + (wg * 2 + half) * p.G * 128;
+    for (int hh = 0; hh < p.G; ++hh) my_acc[hh * 128 + r] = 0.f;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
-    float best = 0.f;
     for (int i = 0; i < n_items; ++i) {
       const int sb2 = i & 1, st = i % kStages;
-      const int q0 = (qt_begin + i % per_head) * 128;
-      const float* bq = sb + st * 128;
+      const int q0 = (qt_begin + i % per_head) * 128 + half * 64;   // first query of this half
+      const float* bq = sb + st * 128 + half * 64;
       tc::mbar_wait(q_full + st, (i / kStages) & 1);      // biases of this item have landed
       tc::mbar_wait(s_full + sb2, (i >> 1) & 1);
       tc::tc_fence_after();
       if (active) {
-        const uint32_t tbase = tmem + (2 * sb2 + wg) * 128 + lane_off;
+        const uint32_t tbase = tmem + (2 * sb2 + wg) * 128 + half * 64 + lane_off;
         const bool cut = !resident && q0 < (t + 1) * 128;   // causal cut inside this block
-        float xa[32], xb[32];
-        tc::tmem_ld32(tbase, xa);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float* x = (c & 1) ? xb : xa;
-          float* xn = (c & 1) ? xa : xb;
+        for (int c = 0; c < 2; ++c) {
+          float x[32];
+          tc::tmem_ld32(tbase + c * 32, x);
           tc::tmem_wait_ld();
-          if (c < 3) tc::tmem_ld32(tbase + (c + 1) * 32, xn);   // next chunk in flight
           if (!cut) score_chunk<false>(x, bq + c * 32, sc2, 0, a0, a1, a2, a3);
           else score_chunk<true>(x, bq + c * 32, sc2, key_idx - (q0 + c * 32), a0, a1, a2, a3);
         }
@@ -450,13 +452,20 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) { tc::mbar_arrive(s_free + sb2); tc::mbar_arrive(q_empty + st); }
-      if ((i + 1) % per_head == 0) {                       // head finished: max over the group
+      if ((i + 1) % per_head == 0) {                       // this half's sum for the head
         const float2 s01 = __fadd2_rn(a0, a1), s23 = __fadd2_rn(a2, a3);
-        best = fmaxf(best, (s01.x + s01.y) + (s23.x + s23.y));
+        my_acc[(i / per_head) * 128 + r] = (s01.x + s01.y) + (s23.x + s23.y);
         a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
       }
     }
-    if (active && r < klen) p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
+    tc::named_bar_sync(1, 512);                           // all halves' per-head sums in smem
+    if (half == 0 && active && r < klen) {
+      const float* h0 = sacc + (wg * 2 + 0) * p.G * 128;
+      const float* h1 = sacc + (wg * 2 + 1) * p.G * 128;
+      float best = 0.f;
+      for (int hh = 0; hh < p.G; ++hh) best = fmaxf(best, h0[hh * 128 + r] + h1[hh * 128 + r]);
+      p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -472,8 +481,7 @@ size_t attn_fwd_tc_smem(int d) {
 }
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
-  (void)G;
-  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + 16 * 8 + 64;
+  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + (size_t)4 * G * 128 * 4 + 16 * 8 + 64;
 }
 
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -496,10 +504,10 @@ void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtens
   const size_t smem = attn_score_tc_smem(d, p.G);
   if (d == 128) {
     cudaFuncSetAttribute(attn_score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<128><<<grid, 384, smem, st>>>(tq, tk, p);
+    attn_score_tc_kernel<128><<<grid, 640, smem, st>>>(tq, tk, p);
   } else {
     cudaFuncSetAttribute(attn_score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<64><<<grid, 384, smem, st>>>(tq, tk, p);
+    attn_score_tc_kernel<64><<<grid, 640, smem, st>>>(tq, tk, p);
   }
 }
 
