@@ -91,7 +91,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
-  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + N + 2) + (N + 3) + 32);
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) + 32);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -104,7 +104,7 @@ Sizes compute_sizes(const cascade_config& c) {
   if (c.dtype == CASCADE_BF16) {
     const size_t bgs = B * Hk;
     size_t ns = (148 * 7 + bgs - 1) / bgs;
-    ns = std::max<size_t>(1, std::min<size_t>(ns, ((S / 128 + N + 2) + 1 + 3) / 4));
+    ns = std::max<size_t>(1, std::min<size_t>(ns, ((S / 128 + 2 * N + 2) + 1 + 3) / 4));
     z.dec_nsplit = (int32_t)ns;
     z.dec_logits = align_up(bgs * (S + 1) * G * 4);
     z.dec_part_o = align_up(bgs * ns * G * d * 4);
@@ -113,8 +113,8 @@ Sizes compute_sizes(const cascade_config& c) {
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
                 z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
-  z.tab_hi = align_up(((S + M) / 64 + 1) * (d / 2) * sizeof(float2));
-  z.tab_lo = align_up(64 * (d / 2) * sizeof(float2));
+  z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(float2));
+  z.tab_lo = align_up(32 * (d / 2) * sizeof(float2));
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
@@ -341,14 +341,14 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     }
     ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(float2),
                           cudaMemcpyHostToDevice) == cudaSuccess;
-    // angle-addition factors for decode: pe = 64 a + b, cos/sin(64 a theta_i) and cos/sin(b theta_i)
-    const size_t nhi = npos / 64 + 1;
-    std::vector<float2> hi(nhi * half), lo(64 * half);
+    // angle-addition factors for decode: pe = 32 a + b, cos/sin(32 a theta_i) and cos/sin(b theta_i)
+    const size_t nhi = npos / 32 + 1;
+    std::vector<float2> hi(nhi * half), lo(32 * half);
     for (int i = 0; i < half; ++i) {
       const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
       for (size_t a = 0; a < nhi; ++a)
-        hi[a * half + i] = make_float2((float)std::cos(64.0 * a * f), (float)std::sin(64.0 * a * f));
-      for (int bb = 0; bb < 64; ++bb)
+        hi[a * half + i] = make_float2((float)std::cos(32.0 * a * f), (float)std::sin(32.0 * a * f));
+      for (int bb = 0; bb < 32; ++bb)
         lo[bb * half + i] = make_float2((float)std::cos(bb * f), (float)std::sin(bb * f));
     }
     ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
@@ -392,7 +392,8 @@ struct Upload {
   const int2* tiles;     // resident key tiles (start slot, valid length)
   int32_t n_tiles;
   const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
-  const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, wrap index)
+  const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
+  int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
 };
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
@@ -434,8 +435,8 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   for (int32_t i = 0; i < h->N; ++i) add_run(h->alpha + i * h->c, pre.counts[i]);
   int32_t* phases = tiles + 2 * nt;                  // (2 nt ints: phases stay 4-aligned + 2 nt)
   for (size_t i = 0; i < P.phase_begin.size(); ++i) phases[i] = P.phase_begin[i];
-  // the same tiles with their rank geometry for decode: pe of key j = pe0 + j, minus c for
-  // j >= jw (a full ring's slots before xi come after its oldest)
+  // the same runs as 128-slot tiles with their rank geometry for decode: pe of key j = pe0 + j;
+  // a tile of a full ring is split where the ring wraps past its oldest slot xi
   const size_t dt_off = pad4(tiles_off + 2 * (size_t)nt + P.phase_begin.size());
   int32_t* dt = buf + dt_off;
   int32_t ndt = 0;
@@ -454,8 +455,10 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
         const int32_t len = std::min(128, cnt - s0);
         const int32_t x0 = h->alpha + i * c + s0;
         if (!full) { add_dec(x0, len, bases[i] + s0, 128); continue; }
-        if (s0 >= xi) add_dec(x0, len, bases[i] + s0 - xi, 128);
-        else add_dec(x0, len, bases[i] + s0 - xi + c, (s0 + len > xi) ? xi - s0 : 128);
+        if (s0 >= xi) { add_dec(x0, len, bases[i] + s0 - xi, 128); continue; }
+        const int32_t before = std::min(len, xi - s0);         // slots s0 .. xi-1: newest part
+        add_dec(x0, before, bases[i] + s0 - xi + c, 128);
+        if (before < len) add_dec(x0 + before, len - before, bases[i], 128);
       }
     }
   }
@@ -475,6 +478,7 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->n_tiles = nt;
   up->phase_begin = L.plan + tiles_off + 2 * nt;
   up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
+  up->n_dec_tiles = ndt;
   return CASCADE_OK;
 }
 
@@ -645,7 +649,7 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
   dp.logits = L.dec_logits; dp.part_o = L.dec_part_o; dp.part_ml = L.dec_part_ml;
   dp.lse2 = L.lse;
-  dp.n_tiles = up.n_tiles;
+  dp.n_tiles = up.n_dec_tiles;
   dp.dec_tiles = up.dec_tiles;
   dp.nsplit = std::min<int32_t>((int32_t)decode_attn_nsplit(dp), h->sz.dec_nsplit);
   const Plan& P = h->plan;

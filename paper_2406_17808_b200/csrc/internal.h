@@ -112,7 +112,7 @@ struct DecodeParams {
   int32_t n_keys;               // n_cached + 1 (the new token)
   int32_t nsplit;
   int32_t n_tiles;              // resident key tiles (the new token is one more)
-  const int4* dec_tiles;        // (start slot, length, pe of key 0, wrap index) per tile
+  const int4* dec_tiles;        // (start slot, length, pe of key 0, unused) per tile
   int64_t t0;                   // stream index of the new token
   float scale_log2;             // softmax scale * log2(e)
   float w0;                     // (1 - gamma): EMA weight of the single row (Alg. 3, m = 1)
@@ -126,8 +126,8 @@ struct DecodeParams {
   int64_t* origin;              // state
   float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
   const float2* tab;            // [npos][D/2] cos/sin(pe theta_i)
-  const float2* tab_hi;         // [npos/64 + 1][D/2] cos/sin(64 a theta_i)
-  const float2* tab_lo;         // [64][D/2] cos/sin(b theta_i)
+  const float2* tab_hi;         // [npos/32 + 1][D/2] cos/sin(32 a theta_i)
+  const float2* tab_lo;         // [32][D/2] cos/sin(b theta_i)
   float* logits;                // [B*Hkv][S_tot + 1][G] log2-domain scaled logits
   float* part_o;                // [B*Hkv][nsplit][G][D]
   float* part_ml;               // [B*Hkv][nsplit][G][2]

@@ -31,41 +31,48 @@ namespace {
 // contiguous in memory) plus a 1-key tile for the new token.
 //   warp 0     producer: TMA of the raw K tile and the V tile (SWIZZLE_128B) + the cos/sin rows
 //              of the tile's 64-position blocks (bulk copies) into a 2-stage ring
-//   warp 1     MMA: S^T[128 keys x 16] = K_rot Q^T, then O^T[128 d x 16] += V^T P^T
+//   warp 1     MMA: S^T[128 keys x 16] = K_rot Q^T (two S^T buffers, so QK(j+1) runs during
+//              softmax(j)), then O^T[128 d x 16] += V^T P^T
 //   warp 2     TMEM allocator
-//   warps 4-7  thread t = key t: rotate the raw key IN PLACE to its rank pe (cos/sin of
-//              (64a + b) theta by angle addition: a-rows from the stage, b-rows resident in
-//              shared memory), round to bf16 (reading Q17); then logits, online softmax, P^T.
-// Tile descriptor (int4, host): start slot, length, pe of key 0, wrap index jw (keys j >= jw
-// of a full ring sit before its oldest slot: pe = pe0 + j - c).
+//   warps 4-7  softmax: thread t = key t: logits, online softmax per head, P^T
+//   warps 8-15 two rotation warpgroups (half of the rotate-half pairs each): rotate every raw
+//              key IN PLACE to its rank pe (cos/sin of (32a + b) theta by angle addition:
+//              a-rows from the stage, b-rows resident), round to bf16 (reading Q17); they run
+//              up to a full ring ahead of the softmax.
+// Tile descriptor (int4, host): start slot, length, pe of key 0 (pe of key j = pe0 + j: the host
+// splits a tile where a full ring wraps past its oldest slot).
 namespace {
-constexpr int kHiRows = 6;                                   // a-rows per tile (<= 3 per pe range)
+constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
+constexpr int kLoRows = 32;                                  // pe = 32 a + b
 constexpr int kLoStride = 64 * 8 + 8;                        // padded bytes per b-row (bank spread)
+constexpr int kDecStages = 3;
 }
 
 template <int G>
-__global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_constant__ CUtensorMap tm_k,
+__global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                              const __grid_constant__ CUtensorMap tm_v,
                                                              DecodeParams p) {
   constexpr int D = 128, HALF = 64;
-  constexpr int kStageBytes = 65536 + kHiRows * 512;
-  extern __shared__ __align__(1024) uint8_t dsm_raw[];
-  uint8_t* dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
-  uint8_t* sStage = dsm;                                    // 2 x [K 32 KB | V 32 KB | hi rows 3 KB]
-  uint8_t* sQ = sStage + 2 * kStageBytes;                   // [16 rows x 128 d] SW128 (2 x 2 KB)
+  // K 32 KB | V 32 KB | a-rows, padded to 1 KB: the next stage's SWIZZLE_128B tiles need 1024-B alignment
+  constexpr int kStageBytes = (65536 + kHiRows * 512 + 1023) / 1024 * 1024;
+  // All shared memory is dynamic (no static variables, so the window starts 1024-B aligned and
+  // three stages fit): stages | Q | P | cos/sin(b theta) rows | small scalars and barriers.
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* sStage = dsm;                                    // kDecStages x [K | V | a-rows]
+  uint8_t* sQ = sStage + kDecStages * kStageBytes;          // [16 rows x 128 d] SW128 (2 x 2 KB)
   uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
-  uint8_t* sLo = sP + 4096;                                 // 64 x kLoStride: cos/sin(b theta_i)
-  __shared__ float sRed[4][G];
-  __shared__ float sCorr[G];
-  __shared__ int sRescale;
-  __shared__ uint32_t sTmem;
-  __shared__ __align__(8) uint64_t bars[8];
-  uint64_t* full = bars + 0;        // [2]
-  uint64_t* empty = bars + 2;       // [2]
-  uint64_t* rot_full = bars + 4;
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* pv_done = bars + 7;
+  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i)
+  float (*sRed)[G] = reinterpret_cast<float (*)[G]>(sLo + kLoRows * kLoStride);   // [4][G]
+  float* sCorr = reinterpret_cast<float*>(sRed + 4);
+  int* sRescale = reinterpret_cast<int*>(sCorr + G);
+  uint32_t* sTmemP = reinterpret_cast<uint32_t*>(sRescale + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sTmemP + 1) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars + 0;        // [3]
+  uint64_t* empty = bars + 3;       // [3]
+  uint64_t* rot_full = bars + 6;    // [3 stages][2 rotation warpgroups]
+  uint64_t* s_full = bars + 12;     // [2] per S^T buffer
+  uint64_t* p_full = bars + 14;     // [2] per S^T buffer
+  uint64_t* pv_done = bars + 16;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bg = blockIdx.x, split = blockIdx.y;
@@ -76,15 +83,14 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
   const int nt = max(0, tend - tbeg);
 
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
-    tc::mbar_init(rot_full, 4);
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(p_full, 4);
+    for (int i = 0; i < kDecStages; ++i) { tc::mbar_init(full + i, 1); tc::mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2 * kDecStages; ++i) tc::mbar_init(rot_full + i, 4);
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
     tc::mbar_init(pv_done, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_v); }
-  if (warp == 2) tc::tmem_alloc<32>(&sTmem);
+  if (warp == 2) tc::tmem_alloc<64>(sTmemP);
   // group queries rotated to pe = n_cached, bf16 (rows >= G zero); cos/sin(b theta) rows
   for (int o = tid; o < 16 * HALF; o += blockDim.x) {
     const int h = o / HALF, i = o - h * HALF;
@@ -100,39 +106,36 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
     *reinterpret_cast<__nv_bfloat16*>(sQ + off) = __float2bfloat16_rn(r1);
     *reinterpret_cast<__nv_bfloat16*>(sQ + 2048 + off) = __float2bfloat16_rn(r2);
   }
-  for (int o = tid; o < 64 * HALF; o += blockDim.x)
+  for (int o = tid; o < kLoRows * HALF; o += blockDim.x)
     *reinterpret_cast<float2*>(sLo + (o / HALF) * kLoStride + (o % HALF) * 8) = p.tab_lo[o];
   for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = sTmem, tS = tmem, tO = tmem + 16;
+  const uint32_t tmem = *sTmemP, tO = tmem + 16;          // S^T buffers at columns 0 and 32
 
-  // per-tile geometry (same on every warp): start slot, length, pe0, wrap index
-  auto tile_info = [&](int ti, int& start, int& len, int& pe0, int& jw) {
+  // per-tile geometry (same on every warp): start slot, length, pe of key 0
+  auto tile_info = [&](int ti, int& start, int& len, int& pe0) {
     if (ti < p.n_tiles) {
       const int4 t4 = p.dec_tiles[ti];
-      start = t4.x; len = t4.y; pe0 = t4.z; jw = t4.w;
+      start = t4.x; len = t4.y; pe0 = t4.z;
     } else {
-      start = p.S_tot; len = 1; pe0 = p.n_keys - 1; jw = 1;     // the new token
+      start = p.S_tot; len = 1; pe0 = p.n_keys - 1;              // the new token
     }
   };
 
   if (warp == 0) {
     if (tc::elect_one()) {
       for (int j = 0; j < nt; ++j) {
-        const int s = j & 1;
-        if (j >= 2) tc::mbar_wait(empty + s, ((j >> 1) - 1) & 1);
-        int start, len, pe0, jw;
-        tile_info(tbeg + j, start, len, pe0, jw);
+        const int s = j % kDecStages;
+        if (j >= kDecStages) tc::mbar_wait(empty + s, ((j / kDecStages) - 1) & 1);
+        int start, len, pe0;
+        tile_info(tbeg + j, start, len, pe0);
         uint8_t* st = sStage + s * kStageBytes;
-        // a-rows of the tile's pe ranges: [pe0, pe0+jw) and [pe0+jw-c, pe0+len-c)
-        const int a0 = pe0 >> 6, a1 = (pe0 + min(jw, len) - 1) >> 6;
-        const int nA = a1 - a0 + 1;
-        int nB = 0, b0 = 0;
-        if (jw < len) { b0 = (pe0 + jw - p.c) >> 6; nB = ((pe0 + len - 1 - p.c) >> 6) - b0 + 1; }
-        const uint32_t bytes = (start < p.S_tot ? 65536u : 0u) + (uint32_t)(nA + nB) * 512u;
+        // a-rows of the tile's pe range [pe0, pe0 + len)
+        const int a0 = pe0 >> 5, nA = ((pe0 + len - 1) >> 5) - a0 + 1;
+        const uint32_t bytes = (start < p.S_tot ? 65536u : 0u) + (uint32_t)nA * 512u;
         tc::mbar_expect_tx(full + s, bytes);
         if (start < p.S_tot) {
           const int row = (int)((long long)bg * p.S_tot + start);
@@ -142,7 +145,6 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
           }
         }
         for (int r = 0; r < nA; ++r) tc::bulk_load(st + 65536 + r * 512, p.tab_hi + (long long)(a0 + r) * HALF, 512, full + s);
-        for (int r = 0; r < nB; ++r) tc::bulk_load(st + 65536 + (3 + r) * 512, p.tab_hi + (long long)(b0 + r) * HALF, 512, full + s);
       }
     }
   } else if (warp == 1) {
@@ -150,18 +152,25 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
       constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 16, 0, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, 16, 0, 1);
       const uint32_t aQ = tc::smem_u32(sQ), aP = tc::smem_u32(sP);
-      for (int j = 0; j < nt; ++j) {
-        const uint32_t st = tc::smem_u32(sStage + (j & 1) * kStageBytes);
-        tc::mbar_wait(rot_full, j & 1);                       // rotated key tile in place
+      auto qk = [&](int j) {
+        const int s = j % kDecStages;
+        const uint32_t st = tc::smem_u32(sStage + s * kStageBytes);
+        tc::mbar_wait(rot_full + 2 * s, (j / kDecStages) & 1);       // both rotated halves in place
+        tc::mbar_wait(rot_full + 2 * s + 1, (j / kDecStages) & 1);
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint64_t da = tc::desc_kmajor_sw128(st + (kk >> 2) * 16384 + (kk & 3) * 32);
           const uint64_t db = tc::desc_kmajor_sw128(aQ + (kk >> 2) * 2048 + (kk & 3) * 32);
-          tc::mma_bf16_ss(tS, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+          tc::mma_bf16_ss(tmem + (j & 1) * 32, da, db, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        tc::mma_commit(s_full);
-        tc::mbar_wait(p_full, j & 1);                         // P^T written (and O^T rescaled)
+        tc::mma_commit(s_full + (j & 1));
+      };
+      if (nt > 0) qk(0);
+      for (int j = 0; j < nt; ++j) {
+        if (j + 1 < nt) qk(j + 1);                          // overlaps softmax(j)
+        const uint32_t st = tc::smem_u32(sStage + (j % kDecStages) * kStageBytes);
+        tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);       // P^T written (and O^T rescaled)
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -170,33 +179,29 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
           tc::mma_bf16_ss(tO, da, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(pv_done);
-        tc::mma_commit(empty + (j & 1));
+        tc::mma_commit(empty + (j % kDecStages));
       }
     }
-  } else if (warp >= 4) {
-    const int t = tid - 128;                                 // key row of the tile = TMEM lane
-    const int w4 = warp - 4;
-    const uint32_t lane_off = (uint32_t)(w4 * 32) << 16;
-    float m_run[G], l_part[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
+  } else if (warp >= 8) {
+    // ---------------- rotation warpgroups ----------------
+    const int t = (tid - 256) & 127;                         // key row of the tile
+    const int rwg = (tid - 256) >> 7;                        // chunks [4 rwg, 4 rwg + 4)
     for (int j = 0; j < nt; ++j) {
-      const int s = j & 1;
+      const int s = j % kDecStages;
       uint8_t* st = sStage + s * kStageBytes;
-      int start, len, pe0, jw;
-      tile_info(tbeg + j, start, len, pe0, jw);
+      int start, len, pe0;
+      tile_info(tbeg + j, start, len, pe0);
       const bool valid = t < len;
-      const int pe = pe0 + t - (t >= jw ? p.c : 0);
-      tc::mbar_wait(full + s, (j >> 1) & 1);
+      const int pe = pe0 + t;
+      tc::mbar_wait(full + s, (j / kDecStages) & 1);
       if (start < p.S_tot) {
         // ---- rotate row t in place: pairs (i, i + 64) live at the same swizzled offset of the
         //      two 64-column blocks ----
-        const int a = pe >> 6;
-        const int hr = t < jw ? a - (pe0 >> 6) : 3 + a - ((pe0 + jw - p.c) >> 6);
+        const int hr = (pe >> 5) - (pe0 >> 5);
         const float2* hi = reinterpret_cast<const float2*>(st + 65536 + (valid ? hr : 0) * 512);
-        const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 63) * kLoStride);
+        const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
 #pragma unroll 2
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = t * 128 + ((c ^ (t & 7)) << 4);
           uint4* pa = reinterpret_cast<uint4*>(st + off);
           uint4* pb = reinterpret_cast<uint4*>(st + 16384 + off);
@@ -210,8 +215,8 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
             for (int u = 0; u < 2; ++u) {
               const int i = c * 8 + 2 * e2 + u;
               const float2 h2 = hi[i], l2 = lo[i];
-              const float cs = h2.x * l2.x - h2.y * l2.y;  // cos((64a + b) theta_i)
-              const float sn = h2.y * l2.x + h2.x * l2.y;  // sin((64a + b) theta_i)
+              const float cs = h2.x * l2.x - h2.y * l2.y;  // cos((32a + b) theta_i)
+              const float sn = h2.y * l2.x + h2.x * l2.y;  // sin((32a + b) theta_i)
               const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
               const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
               r[u] = x1 * cs - x2 * sn;
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
       } else {
         // ---- the new token: key row 0 from the input, rotated to n_cached; rows >= 1 zero ----
         const int off_base = t * 128;
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = off_base + ((c ^ (t & 7)) << 4);
           uint4 ka = make_uint4(0u, 0u, 0u, 0u), kb2 = ka, va = ka, vb = ka;
           if (t == 0) {
@@ -262,12 +267,25 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
       }
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(rot_full);
+      if (lane == 0) tc::mbar_arrive(rot_full + 2 * s + rwg);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax warpgroup ----------------
+    const int t = tid - 128;                                 // key = TMEM lane
+    const int w4 = warp & 3;
+    const uint32_t lane_off = (uint32_t)(w4 * 32) << 16;
+    float m_run[G], l_part[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
+    for (int j = 0; j < nt; ++j) {
+      int start, len, pe0;
+      tile_info(tbeg + j, start, len, pe0);
+      const bool valid = t < len;
       // ---- logits, block max per head, P^T ----
-      tc::mbar_wait(s_full, j & 1);
+      tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc::tc_fence_after();
       float sv[16];
-      tc::tmem_ld16(tS + lane_off, sv);
+      tc::tmem_ld16(tmem + (j & 1) * 32 + lane_off, sv);
       tc::tmem_wait_ld();
       float lg[G];
 #pragma unroll
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
           any |= (j > 0 && cr != 1.f);
           sRed[0][h] = mn;
         }
-        sRescale = any;
+        *sRescale = any;
       }
       if (j >= 1) tc::mbar_wait(pv_done, (j - 1) & 1);      // sP free, O^T holds tiles < j
       tc::named_bar_sync(1, 128);
@@ -312,7 +330,7 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
         *reinterpret_cast<__nv_bfloat16*>(sP + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
             __float2bfloat16_rn(pv);
       }
-      if (sRescale) {                                        // O^T column h *= corr_h (lane = d)
+      if (*sRescale) {                                       // O^T column h *= corr_h (lane = d)
         float ov[16];
         tc::tmem_ld16(tO + lane_off, ov);
         tc::tmem_wait_ld();
@@ -325,9 +343,10 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
       tc::tc_fence_before();
       tc::named_bar_sync(1, 128);                            // sRed / sCorr reads done
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
+      if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
     }
     // ---- split results ----
+    {
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float v = l_part[h];
@@ -348,12 +367,13 @@ __global__ void __launch_bounds__(256, 1) decode_attn_kernel(const __grid_consta
     tc::tmem_wait_ld();
 #pragma unroll
     for (int h = 0; h < G; ++h) p.part_o[(pbase + h) * D + t] = nt > 0 ? ov[h] : 0.f;
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<32>(tmem);
+    tc::tmem_dealloc<64>(tmem);
   }
 }
 
@@ -461,9 +481,10 @@ size_t decode_attn_nsplit(const DecodeParams& p) {
 
 template <int G>
 void launch_attn(const DecodeParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
-  const size_t smem = 1024 + 2 * (65536 + kHiRows * 512) + 4096 + 4096 + 64 * kLoStride;
+  const size_t smem = kDecStages * ((65536 + kHiRows * 512 + 1023) / 1024 * 1024) + 4096 + 4096 +
+                      kLoRows * kLoStride + 4 * G * 4 + G * 4 + 8 + 8 + 17 * 8;
   cudaFuncSetAttribute(decode_attn_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  decode_attn_kernel<G><<<dim3(p.B * p.Hkv, p.nsplit), 256, smem, st>>>(tk, tv, p);
+  decode_attn_kernel<G><<<dim3(p.B * p.Hkv, p.nsplit), 512, smem, st>>>(tk, tv, p);
 }
 
 void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
