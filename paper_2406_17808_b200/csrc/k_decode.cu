@@ -411,18 +411,32 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
   double* mu = p.mu + (long long)bg * p.S_tot;
   float* s_out = p.s + (long long)bg * (p.S_tot + 1);
   const float* lg = p.logits + (long long)bg * (p.S_tot + 1) * p.G;
-  // 1. exact mass + fold for every valid slot; the new token's mass lands at S_tot
-  for (int x = tid; x <= p.S_tot; x += blockDim.x) {
-    bool valid;
-    if (x == p.S_tot) valid = true;
-    else if (x < p.alpha) valid = x < p.sink_pre;
-    else { const int i = (x - p.alpha) / p.c; valid = (x - p.alpha - i * p.c) < p.counts[i]; }
-    if (!valid) { s_out[x] = 0.f; continue; }
+  // 1. exact mass + fold for every valid slot, run by run (sinks, C_1 .. C_N); the new token's
+  //    mass lands at S_tot.  Empty slots keep s = 0 (zeroed when the layer was reset / init).
+  const float4* lg4 = reinterpret_cast<const float4*>(lg);
+  for (int run = 0; run <= p.N; ++run) {
+    const int beg = run == 0 ? 0 : p.alpha + (run - 1) * p.c;
+    const int len = run == 0 ? p.sink_pre : p.counts[run - 1];
+    const int cap = run == 0 ? p.alpha : p.c;
+    for (int o = tid; o < cap; o += blockDim.x) {
+      const int x = beg + o;
+      if (o >= len) { s_out[x] = 0.f; continue; }
+      float best = 0.f;
+      if (p.G == 4) {
+        const float4 l = lg4[x];
+        best = fmaxf(fmaxf(exp2f(l.x - sl[0]), exp2f(l.y - sl[1])), fmaxf(exp2f(l.z - sl[2]), exp2f(l.w - sl[3])));
+      } else {
+        for (int h = 0; h < p.G; ++h) best = fmaxf(best, exp2f(lg[(long long)x * p.G + h] - sl[h]));
+      }
+      const float sv = p.w0 * best;
+      s_out[x] = sv;
+      mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)sv);
+    }
+  }
+  if (tid == 0) {
     float best = 0.f;
-    for (int h = 0; h < p.G; ++h) best = fmaxf(best, exp2f(lg[(long long)x * p.G + h] - sl[h]));
-    const float sv = p.w0 * best;
-    s_out[x] = sv;
-    if (x < p.S_tot) mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)sv);
+    for (int h = 0; h < p.G; ++h) best = fmaxf(best, exp2f(lg[(long long)p.S_tot * p.G + h] - sl[h]));
+    s_out[p.S_tot] = p.w0 * best;
   }
   __syncthreads();
   // 2. selections (depth order), 3. moves deepest sub-cache first -- one warp, sequential
