@@ -280,7 +280,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
 // 32 columns of one key row: acc += exp2(S * scale*log2e - b_q), packed f32x2 FMA/FADD,
 // four independent accumulators.  CUT: column c only counts when c >= cut_from (query index
 // >= key index inside the chunk's causal block).
-template <bool CUT>
+template <bool CUT, int EMU, int DEG>
 __device__ __forceinline__ void score_chunk(const float* x, const float* bq, float2 sc2, int cut_from,
                                             float2& a0, float2& a1, float2& a2, float2& a3) {
   const float4* b4 = reinterpret_cast<const float4*>(bq);
@@ -289,10 +289,11 @@ __device__ __forceinline__ void score_chunk(const float* x, const float* bq, flo
     const float4 bb = b4[e >> 2];
     const float2 t0 = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, make_float2(-bb.x, -bb.y));
     const float2 t1 = __ffma2_rn(make_float2(x[e + 2], x[e + 3]), sc2, make_float2(-bb.z, -bb.w));
-    // 6 of every 16 exp2 pairs on the FMA pipe (degree-4 polynomial), the rest on MUFU
-    const int step = e >> 2;
-    float2 p0 = (step & 3) == 3 ? tc::exp2_poly2<4>(t0) : make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
-    float2 p1 = (step & 1) ? tc::exp2_poly2<4>(t1) : make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
+    // EMU of every 16 exp2 pairs on the FMA pipe (degree-DEG polynomial), the rest on MUFU
+    const int q0i = (e >> 1), q1i = (e >> 1) + 1;           // pair indices 0..15 of this chunk
+    const bool e0 = ((q0i * EMU) % 16) + EMU >= 16, e1 = ((q1i * EMU) % 16) + EMU >= 16;
+    float2 p0 = e0 ? tc::exp2_poly2<DEG>(t0) : make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
+    float2 p1 = e1 ? tc::exp2_poly2<DEG>(t1) : make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
     if (CUT) {
       p0.x = e + 0 >= cut_from ? p0.x : 0.f;
       p0.y = e + 1 >= cut_from ? p0.y : 0.f;
@@ -311,7 +312,7 @@ __device__ __forceinline__ void score_chunk(const float* x, const float* bq, flo
 // (half, w) reads key tile w's S^T columns [64 half, 64 half + 64) (thread r = key r = TMEM
 // lane r), so every SMSP has four exp2 warps to hide MUFU/TMEM latency.  Items are
 // (q-head, q-tile); the two column halves meet in shared memory per head before the max.
-template <int D>
+template <int D, int EMU, int DEG>
 __global__ void __launch_bounds__(640, 1)
 attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      TcParams p) {
@@ -445,8 +446,8 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
           float x[32];
           tc::tmem_ld32(tbase + c * 32, x);
           tc::tmem_wait_ld();
-          if (!cut) score_chunk<false>(x, bq + c * 32, sc2, 0, a0, a1, a2, a3);
-          else score_chunk<true>(x, bq + c * 32, sc2, key_idx - (q0 + c * 32), a0, a1, a2, a3);
+          if (!cut) score_chunk<false, EMU, DEG>(x, bq + c * 32, sc2, 0, a0, a1, a2, a3);
+          else score_chunk<true, EMU, DEG>(x, bq + c * 32, sc2, key_idx - (q0 + c * 32), a0, a1, a2, a3);
         }
       }
       tc::tc_fence_before();
@@ -502,12 +503,16 @@ void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtens
                           cudaStream_t st) {
   dim3 grid((p.n_res_tiles + 1) / 2 + ((p.m + 127) / 128 + 1) / 2, p.B * p.Hkv);
   const size_t smem = attn_score_tc_smem(d, p.G);
+  // exp2 pairs on the FMA pipe per 16 (degree-4 polynomial): measured 2.50 / 2.30 / 2.25 / 2.16 /
+  // 2.20 / 2.21 / 2.44 ms per steady-state chunk for 0 / 2 / 3 / 4 / 5 / 6 / 8 (scripts/kbench.py)
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 640, smem, st>>>(tq, tk, p);
+  };
   if (d == 128) {
-    cudaFuncSetAttribute(attn_score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<128><<<grid, 640, smem, st>>>(tq, tk, p);
+    go(attn_score_tc_kernel<128, 4, 4>);
   } else {
-    cudaFuncSetAttribute(attn_score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attn_score_tc_kernel<64><<<grid, 640, smem, st>>>(tq, tk, p);
+    go(attn_score_tc_kernel<64, 4, 4>);
   }
 }
 
