@@ -211,3 +211,27 @@ def test_layers_are_independent_across_streams():
         st = g.state(l)
         for key in ("origin", "mu", "k", "v", "pe"):
             assert torch.equal(st[key], solo[l][2][key]), key
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_ragged_chunks_tensor_core_path(d):
+    """bf16 tcgen05 passes with ragged strides (partial 128-row query and key tiles, a chunk
+    longer than the sub-cache so rings wrap within a call) and head_dim 64/128, vs the oracle."""
+    cfg = C.CascadeConfig(batch=2, num_q_heads=4, num_kv_heads=2, head_dim=d, sink_size=5, cache_size=384,
+                          num_cascades=3, max_stride=300, dtype="bf16")
+    syn = Synth(2, 4, 2, d, seed=200 + d)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    start = 0
+    for m in [200, 77, 128, 300, 1, 255, 129]:
+        q, k, v = syn.chunk(start, m)
+        start += m
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        s_gpu = gpu.last_scores(0)
+        O_ref, s_ref = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL["bf16"], m
+        np.testing.assert_allclose(_np(s_gpu), s_ref, rtol=S_RTOL, atol=1e-30)
+        _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
+    margins = orc.select_margins()
+    assert margins.size == 0 or margins.min() > 1e-3
