@@ -32,6 +32,9 @@ struct LayerBufs {
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
   float* dec_logits; float* dec_part_o; float* dec_part_ml;
+  uint32_t* maint_done;     // [(N+1) * B*Hkv] cumulative completed maintenance blocks, then the ticket
+  uint32_t maint_cum[CASCADE_MAX_LEVELS + 1];   // host copy: items launched per phase (wrapping)
+  uint32_t maint_tickets;   // host copy: maintenance blocks launched (wrapping)
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
   CUtensorMap tm_kraw;                    // TMA map of the pre-RoPE key state (decode)
 };
@@ -68,7 +71,7 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 
 struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
-  size_t dec_logits, dec_part_o, dec_part_ml;
+  size_t dec_logits, dec_part_o, dec_part_ml, maint_done;
   int32_t dec_nsplit;
   size_t per_layer;
   size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
@@ -91,7 +94,8 @@ Sizes compute_sizes(const cascade_config& c) {
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
-  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) + 32);
+  z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
+                          5 * (S / kMaintSlots + 2 * (N + 1) * M / kMaintMoves + 2 * N + 4) + 48);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -110,8 +114,9 @@ Sizes compute_sizes(const cascade_config& c) {
     z.dec_part_o = align_up(bgs * ns * G * d * 4);
     z.dec_part_ml = align_up(bgs * ns * G * 2 * 4);
   }
+  z.maint_done = align_up(((N + 1) * B * Hk + 1) * 4);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml;
+                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_done;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(float2));
   z.tab_lo = align_up(32 * (d / 2) * sizeof(float2));
@@ -290,6 +295,9 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.dec_logits = reinterpret_cast<float*>(take(sz.dec_logits));
     L.dec_part_o = reinterpret_cast<float*>(take(sz.dec_part_o));
     L.dec_part_ml = reinterpret_cast<float*>(take(sz.dec_part_ml));
+    L.maint_done = reinterpret_cast<uint32_t*>(take(sz.maint_done));
+    std::memset(L.maint_cum, 0, sizeof(L.maint_cum));
+    L.maint_tickets = 0;
   }
   h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
@@ -312,6 +320,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     ok = ok && cudaMemsetAsync(L.k_raw, 0, sz.k_raw) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.v, 0, sz.v) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.s, 0, sz.s) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.maint_done, 0, sz.maint_done) == cudaSuccess;
     // scratch read by masked lanes of the MMAs must hold finite values (0 * NaN = NaN)
     ok = ok && cudaMemsetAsync(L.q_rot, 0, sz.q_rot) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.k_rot, 0, sz.k_rot) == cudaSuccess;
@@ -394,6 +403,10 @@ struct Upload {
   const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
   const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
   int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
+  const int4* maint_items;     // (slot_lo, slot_len, move_begin, move_end) per maintenance block
+  const int32_t* maint_phase;  // phase of each item (0 .. N-1 = C_N .. C_1, N = sinks)
+  int32_t n_maint_items;
+  int32_t maint_per_phase[CASCADE_MAX_LEVELS + 1];   // items per phase
 };
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
@@ -462,7 +475,41 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
       }
     }
   }
-  const size_t total = dt_off + 4 * (size_t)ndt;
+  // maintenance items, phase by phase (C_N .. C_1, sinks): ranges of <= kMaintSlots slots
+  // holding <= kMaintMoves of the phase's moves (sorted by destination); ranges with neither
+  // a resident to fold nor a move are dropped
+  const size_t mi_off = pad4(dt_off + 4 * (size_t)ndt);
+  int32_t* mi = buf + mi_off;
+  int32_t nmi = 0;
+  std::vector<int32_t> mi_phase;
+  for (int32_t ph = 0; ph <= h->N; ++ph) {
+    const int32_t lvl = h->N - 1 - ph;
+    const int32_t lo = ph < h->N ? h->alpha + lvl * h->c : 0;
+    const int32_t hi = lo + (ph < h->N ? h->c : h->alpha);
+    const int32_t vend = ph < h->N ? lo + pre.counts[lvl] : pre.sink_count;
+    int32_t e = P.phase_begin[ph];
+    const int32_t e_end = P.phase_begin[ph + 1];
+    int32_t items = 0;
+    for (int32_t a = lo; a < hi;) {
+      int32_t end = std::min(a + kMaintSlots, hi);
+      int32_t e2 = e;
+      while (e2 < e_end && P.mov[2 * e2] < end && e2 - e < kMaintMoves) ++e2;
+      if (e2 < e_end && P.mov[2 * e2] < end) end = P.mov[2 * e2];    // move budget reached
+      if (a < vend || e2 > e) {
+        mi[4 * nmi] = a; mi[4 * nmi + 1] = end - a; mi[4 * nmi + 2] = e; mi[4 * nmi + 3] = e2;
+        mi_phase.push_back(ph);
+        ++nmi;
+        ++items;
+      }
+      a = end;
+      e = e2;
+    }
+    up->maint_per_phase[ph] = items;
+  }
+  int32_t* mip = mi + 4 * nmi;
+  for (int32_t i = 0; i < nmi; ++i) mip[i] = mi_phase[i];
+  const size_t total = mi_off + 5 * (size_t)nmi;
+  if (total > (size_t)h->sz.plan_ints) return CASCADE_ERR_WORKSPACE;   // capacity formula broken
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -479,25 +526,36 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->phase_begin = L.plan + tiles_off + 2 * nt;
   up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
   up->n_dec_tiles = ndt;
+  up->maint_items = reinterpret_cast<const int4*>(L.plan + mi_off);
+  up->maint_phase = L.plan + mi_off + 4 * nmi;
+  up->n_maint_items = nmi;
   return CASCADE_OK;
 }
 
 template <typename T>
-void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const PlanDev& pd,
+void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up,
                         const T* k, const T* v, const float* s, cudaStream_t st) {
   const Plan& P = h->plan;
+  const PlanDev& pd = up.pd;
   ProfScope ps(h, 3, st);
-  launch_ema_fold(g, L.mu, s, st); ++h->launches;
   for (size_t dpt = 0; dpt + 1 < P.depth_begin.size(); ++dpt) {
     launch_select_resolve(g, pd, P.depth_begin[dpt], P.depth_begin[dpt + 1], L.mu, s, st);
     ++h->launches;
   }
-  StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin};
-  for (size_t ph = 0; ph + 1 < P.phase_begin.size(); ++ph) {
-    if (P.phase_begin[ph + 1] == P.phase_begin[ph]) continue;
-    launch_moves<T>(g, pd, P.phase_begin[ph], P.phase_begin[ph + 1], sd, k, v, s, st);
-    ++h->launches;
+  MaintItems it{};
+  it.items = up.maint_items;
+  it.phase = up.maint_phase;
+  it.done = L.maint_done;
+  it.ticket = L.maint_done + (size_t)(g.N + 1) * g.B * g.Hkv;
+  it.ticket_base = L.maint_tickets;
+  L.maint_tickets += (uint32_t)up.n_maint_items * (uint32_t)(g.B * g.Hkv);
+  for (int ph = 0; ph <= g.N; ++ph) {
+    L.maint_cum[ph] += (uint32_t)up.maint_per_phase[ph];
+    it.expect[ph] = L.maint_cum[ph];
   }
+  StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin};
+  launch_maint<T>(g, pd, it, up.n_maint_items, sd, k, v, s, st);
+  ++h->launches;
   // algorithmic bytes: EMA 20 B per resident (mu r/w + s), each final row write moves
   // K, V, mu, origin once (read + write)
   const double bg = (double)g.B * g.Hkv;
@@ -559,7 +617,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     }
   }
   h->launches += 3;
-  launch_maintenance<T>(h, g, L, pd, k, v, L.s, st);
+  launch_maintenance<T>(h, g, L, up, k, v, L.s, st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;   // commit the mirror
   h->m_last[layer] = m;
@@ -681,10 +739,10 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   if (rc != CASCADE_OK) return rc;
   const PlanDev& pd = up.pd;
   if (h->cfg.dtype == CASCADE_BF16)
-    launch_maintenance<__nv_bfloat16>(h, g, L, pd, static_cast<const __nv_bfloat16*>(k),
+    launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
                                       static_cast<const __nv_bfloat16*>(v), s, st);
   else
-    launch_maintenance<float>(h, g, L, pd, static_cast<const float*>(k), static_cast<const float*>(v), s, st);
+    launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k), static_cast<const float*>(v), s, st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;
   h->m_last[layer] = 0;
@@ -709,8 +767,11 @@ cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
-      cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess)
+      cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess ||
+      cudaMemsetAsync(L.maint_done, 0, h->sz.maint_done, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
+  std::memset(L.maint_cum, 0, sizeof(L.maint_cum));
+  L.maint_tickets = 0;
   h->mirrors[layer] = cascade_mirror{};
   h->m_last[layer] = 0;
   return CASCADE_OK;

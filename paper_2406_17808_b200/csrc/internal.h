@@ -78,13 +78,23 @@ template <typename T>
 void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, const float* lse,
                             const float* w, float* s, cudaStream_t st);
 
-void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t st);
 
 void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end,
                            const double* mu, const float* s, cudaStream_t st);
 
+// One maintenance launch per chunk (k_maint.cu): items = (phase, slice) in phase order.
+constexpr int kMaintSlots = 512;   // slots folded per maintenance block (2 per thread)
+constexpr int kMaintMoves = 32;    // rows written per maintenance block (4 per warp)
+struct MaintItems {
+  const int4* items;          // [n_items] slot_lo, slot_len, move_begin, move_end (phase-major)
+  const int32_t* phase;       // [n_items] 0 .. N-1 = C_N .. C_1, N = sinks
+  uint32_t* done;             // [(N+1) * B*Hkv] cumulative completed blocks per (phase, b*g), wrapping
+  uint32_t* ticket;           // block start order (blocks only wait on blocks that started earlier)
+  uint32_t ticket_base;       // ticket value of this launch's first block
+  uint32_t expect[CASCADE_MAX_LEVELS + 1];   // done[p] once phase p of this chunk is complete
+};
 template <typename T>
-void launch_moves(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end, StateDev<T> st_,
+void launch_maint(const Geometry& g, const PlanDev& p, const MaintItems& it, int n_items, StateDev<T> sd,
                   const T* k_in, const T* v_in, const float* s, cudaStream_t st);
 
 void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
