@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <type_traits>
@@ -23,6 +24,12 @@ constexpr int kRing = 8;   // pinned schedule staging buffers in flight
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
+// maintenance items per chunk: every item but the last of a phase holds kMaintMoves moves,
+// and a chunk of M tokens touches <= 2 (N + 1) M slots
+int32_t max_maint_items(int32_t N, int32_t M) { return 2 * (N + 1) * M / kMaintMoves + N + 2; }
+// words of maint_ctl before the flags: one ticket per (b, g) (padded to even), the moved count
+size_t maint_ctl_head(size_t BG) { return ((BG + 1) & ~size_t(1)) + 2 * BG; }
+
 size_t elem_size(int32_t dtype) { return dtype == CASCADE_BF16 ? 2 : 4; }
 
 struct LayerBufs {
@@ -32,9 +39,10 @@ struct LayerBufs {
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
   float* dec_logits; float* dec_part_o; float* dec_part_ml;
-  uint32_t* maint_done;     // [(N+1) * B*Hkv] cumulative completed maintenance blocks, then the ticket
-  uint32_t maint_cum[CASCADE_MAX_LEVELS + 1];   // host copy: items launched per phase (wrapping)
+  uint32_t* maint_ctl;      // per-(b, g) block tickets, the 64-bit count of rows actually
+                            // rewritten, then per-(item, b*g) epoch flags (MaintItems)
   uint32_t maint_tickets;   // host copy: maintenance blocks launched (wrapping)
+  uint32_t maint_epoch;     // host copy: epoch of the last maintenance launch (never 0)
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
   CUtensorMap tm_kraw;                    // TMA map of the pre-RoPE key state (decode)
 };
@@ -71,7 +79,7 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 
 struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
-  size_t dec_logits, dec_part_o, dec_part_ml, maint_done;
+  size_t dec_logits, dec_part_o, dec_part_ml, maint_ctl;
   int32_t dec_nsplit;
   size_t per_layer;
   size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
@@ -95,7 +103,7 @@ Sizes compute_sizes(const cascade_config& c) {
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
-                          5 * (S / kMaintSlots + 2 * (N + 1) * M / kMaintMoves + 2 * N + 4) + 48);
+                          4 * (1 + kMaintMoves) * max_maint_items(N, M) + 4 * 2 * (N + 1) * M + 48);
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -114,9 +122,9 @@ Sizes compute_sizes(const cascade_config& c) {
     z.dec_part_o = align_up(bgs * ns * G * d * 4);
     z.dec_part_ml = align_up(bgs * ns * G * 2 * 4);
   }
-  z.maint_done = align_up(((N + 1) * B * Hk + 1) * 4);
+  z.maint_ctl = align_up(4 * maint_ctl_head(B * Hk) + (size_t)max_maint_items(N, M) * B * Hk * 4);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_done;
+                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_ctl;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(float2));
   z.tab_lo = align_up(32 * (d / 2) * sizeof(float2));
@@ -153,6 +161,15 @@ struct cascade_handle {
   struct Rec { cudaEvent_t a, b; double work; };
   std::vector<Rec> recs[CASCADE_PROFILE_CLASSES];
   std::vector<cudaEvent_t> ev_pool;
+  uint64_t moved_seen;      // sum over layers of the device moved-row counters at the last read
+  uint64_t moved_chunk;     // chunk-row moves launched (each always rewrites its row)
+  // maintenance planning scratch: writer item of each destination slot of the current chunk
+  std::vector<int32_t> wr_item;
+  std::vector<uint32_t> wr_stamp;
+  uint32_t wr_cur;
+  std::vector<int32_t> maint_reads;
+  std::vector<int4> maint_chunk;
+  bool maint_split;         // chunk-row moves in their own launch (CASCADE_MAINT_SPLIT, default 0)
 };
 
 namespace {
@@ -274,9 +291,15 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->c = cfg->cache_size / cfg->num_cascades;
   h->S_tot = h->alpha + cfg->cache_size;
   h->planner.configure(h->alpha, h->N, h->c);
+  h->wr_item.assign(h->S_tot, 0);
+  h->wr_stamp.assign(h->S_tot, 0u);
+  h->wr_cur = 0;
   h->launches = 0;
   h->ring_pos = 0;
   h->profiling = false;
+  h->moved_seen = 0;
+  { const char* e = std::getenv("CASCADE_MAINT_SPLIT"); h->maint_split = e && std::atoi(e) != 0; }
+  h->moved_chunk = 0;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
 
   char* p = static_cast<char*>(d_ws);
@@ -295,9 +318,9 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.dec_logits = reinterpret_cast<float*>(take(sz.dec_logits));
     L.dec_part_o = reinterpret_cast<float*>(take(sz.dec_part_o));
     L.dec_part_ml = reinterpret_cast<float*>(take(sz.dec_part_ml));
-    L.maint_done = reinterpret_cast<uint32_t*>(take(sz.maint_done));
-    std::memset(L.maint_cum, 0, sizeof(L.maint_cum));
+    L.maint_ctl = reinterpret_cast<uint32_t*>(take(sz.maint_ctl));
     L.maint_tickets = 0;
+    L.maint_epoch = 0;
   }
   h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
@@ -320,7 +343,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     ok = ok && cudaMemsetAsync(L.k_raw, 0, sz.k_raw) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.v, 0, sz.v) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.s, 0, sz.s) == cudaSuccess;
-    ok = ok && cudaMemsetAsync(L.maint_done, 0, sz.maint_done) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(L.maint_ctl, 0, sz.maint_ctl) == cudaSuccess;
     // scratch read by masked lanes of the MMAs must hold finite values (0 * NaN = NaN)
     ok = ok && cudaMemsetAsync(L.q_rot, 0, sz.q_rot) == cudaSuccess;
     ok = ok && cudaMemsetAsync(L.k_rot, 0, sz.k_rot) == cudaSuccess;
@@ -403,10 +426,10 @@ struct Upload {
   const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
   const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
   int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
-  const int4* maint_items;     // (slot_lo, slot_len, move_begin, move_end) per maintenance block
-  const int32_t* maint_phase;  // phase of each item (0 .. N-1 = C_N .. C_1, N = sinks)
+  const int4* maint_rec;       // maintenance item records (MaintItems::rec)
   int32_t n_maint_items;
-  int32_t maint_per_phase[CASCADE_MAX_LEVELS + 1];   // items per phase
+  const int4* maint_chunk;     // moves that read no resident slot (MaintItems::chunk)
+  int32_t n_maint_chunk;
 };
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
@@ -475,40 +498,70 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
       }
     }
   }
-  // maintenance items, phase by phase (C_N .. C_1, sinks): ranges of <= kMaintSlots slots
-  // holding <= kMaintMoves of the phase's moves (sorted by destination); ranges with neither
-  // a resident to fold nor a move are dropped
+  // maintenance items, phase by phase (C_N .. C_1, sinks): runs of <= kMaintMoves of the
+  // phase's moves (sorted by destination) of which <= kMaintStaged read a resident slot
   const size_t mi_off = pad4(dt_off + 4 * (size_t)ndt);
-  int32_t* mi = buf + mi_off;
+  int4* rec = reinterpret_cast<int4*>(buf + mi_off);
   int32_t nmi = 0;
-  std::vector<int32_t> mi_phase;
+  const int32_t S_tot = h->S_tot;
+  // concrete slots a plan reference reads (a selection reads both operands)
+  std::vector<int32_t>& rd = h->maint_reads;
+  auto reads = [&](int32_t ref, auto&& self) -> void {
+    if (ref >= 0) { if (ref < S_tot) rd.push_back(ref); return; }
+    const int32_t k = -ref - 1;
+    self(P.sel[3 * k + 1], self);
+    self(P.sel[3 * k + 2], self);
+  };
+  if (++h->wr_cur == 0) { std::fill(h->wr_stamp.begin(), h->wr_stamp.end(), 0u); h->wr_cur = 1; }
+  std::vector<int4>& chunk_moves = h->maint_chunk;
+  chunk_moves.clear();
   for (int32_t ph = 0; ph <= h->N; ++ph) {
-    const int32_t lvl = h->N - 1 - ph;
-    const int32_t lo = ph < h->N ? h->alpha + lvl * h->c : 0;
-    const int32_t hi = lo + (ph < h->N ? h->c : h->alpha);
-    const int32_t vend = ph < h->N ? lo + pre.counts[lvl] : pre.sink_count;
-    int32_t e = P.phase_begin[ph];
-    const int32_t e_end = P.phase_begin[ph + 1];
-    int32_t items = 0;
-    for (int32_t a = lo; a < hi;) {
-      int32_t end = std::min(a + kMaintSlots, hi);
-      int32_t e2 = e;
-      while (e2 < e_end && P.mov[2 * e2] < end && e2 - e < kMaintMoves) ++e2;
-      if (e2 < e_end && P.mov[2 * e2] < end) end = P.mov[2 * e2];    // move budget reached
-      if (a < vend || e2 > e) {
-        mi[4 * nmi] = a; mi[4 * nmi + 1] = end - a; mi[4 * nmi + 2] = e; mi[4 * nmi + 3] = e2;
-        mi_phase.push_back(ph);
-        ++nmi;
-        ++items;
+    int32_t open = -1, n = 0;
+    for (int32_t e = P.phase_begin[ph]; e < P.phase_begin[ph + 1]; ++e) {
+      const int32_t dst = P.mov[2 * e], ref = P.mov[2 * e + 1];
+      int32_t cand = 0, inc = 0;
+      if (ref < 0) { cand = P.sel[3 * (-ref - 1) + 1]; inc = P.sel[3 * (-ref - 1) + 2]; }
+      rd.clear();
+      reads(ref, reads);
+      if (rd.empty() && h->maint_split) {     // reads no resident slot: chunk_moves_kernel
+        chunk_moves.push_back(make_int4(dst, ref, cand, inc));
+        continue;
       }
-      a = end;
-      e = e2;
+      if (open < 0 || n == kMaintMoves) {
+        if (open >= 0) rec[open * (1 + kMaintMoves)].x = n;
+        open = nmi++;
+        rec[open * (1 + kMaintMoves)] = make_int4(0, 0, 0, ph);
+        n = 0;
+      }
+      rec[open * (1 + kMaintMoves) + 1 + n] = make_int4(dst, ref, cand, inc);
+      ++n;
+      h->wr_stamp[dst] = h->wr_cur;
+      h->wr_item[dst] = open;
     }
-    up->maint_per_phase[ph] = items;
+    if (open >= 0) rec[open * (1 + kMaintMoves)].x = n;
   }
-  int32_t* mip = mi + 4 * nmi;
-  for (int32_t i = 0; i < nmi; ++i) mip[i] = mi_phase[i];
-  const size_t total = mi_off + 5 * (size_t)nmi;
+  // hazards: item J reads slot x that item W overwrites -> W waits for J's "loaded" flag.
+  // Readers sit in deeper sub-caches, i.e. earlier items (a block only waits on blocks that
+  // started before it); anything else is a planner bug.
+  for (int32_t J = 0; J < nmi; ++J) {
+    const int4 hd = rec[J * (1 + kMaintMoves)];
+    for (int32_t j = 0; j < hd.x; ++j) {
+      rd.clear();
+      reads(rec[J * (1 + kMaintMoves) + 1 + j].y, reads);
+      for (int32_t x : rd) {
+        if (h->wr_stamp[x] != h->wr_cur) continue;
+        const int32_t W = h->wr_item[x];
+        if (W == J) continue;
+        if (W < J) return CASCADE_ERR_UNSUPPORTED;
+        int4& hw = rec[W * (1 + kMaintMoves)];
+        if (hw.y == hw.z) { hw.y = J; hw.z = J + 1; }
+        else { hw.y = std::min(hw.y, J); hw.z = std::max(hw.z, J + 1); }
+      }
+    }
+  }
+  const size_t cm_off = mi_off + 4 * (1 + kMaintMoves) * (size_t)nmi;
+  std::memcpy(buf + cm_off, chunk_moves.data(), chunk_moves.size() * sizeof(int4));
+  const size_t total = cm_off + 4 * chunk_moves.size();
   if (total > (size_t)h->sz.plan_ints) return CASCADE_ERR_WORKSPACE;   // capacity formula broken
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -526,41 +579,70 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->phase_begin = L.plan + tiles_off + 2 * nt;
   up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
   up->n_dec_tiles = ndt;
-  up->maint_items = reinterpret_cast<const int4*>(L.plan + mi_off);
-  up->maint_phase = L.plan + mi_off + 4 * nmi;
+  up->maint_rec = reinterpret_cast<const int4*>(L.plan + mi_off);
   up->n_maint_items = nmi;
+  up->maint_chunk = reinterpret_cast<const int4*>(L.plan + cm_off);
+  up->n_maint_chunk = (int32_t)chunk_moves.size();
   return CASCADE_OK;
+}
+
+unsigned long long* maint_moved_ptr(cascade_handle* h, LayerBufs& L) {
+  const size_t BG = (size_t)h->cfg.batch * h->cfg.num_kv_heads;
+  return reinterpret_cast<unsigned long long*>(L.maint_ctl + maint_ctl_head(BG) - 2 * BG);
+}
+
+uint64_t moved_total(cascade_handle* h) {
+  uint64_t tot = 0;
+  for (auto& L : h->layers) {
+    const size_t BG = (size_t)h->cfg.batch * h->cfg.num_kv_heads;
+    std::vector<unsigned long long> v(BG);
+    cudaMemcpy(v.data(), maint_moved_ptr(h, L), 8 * BG, cudaMemcpyDeviceToHost);
+    for (auto x : v) tot += x;
+  }
+  tot += h->moved_chunk;   // chunk-row moves always move: counted at launch
+  return tot;
 }
 
 template <typename T>
 void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up,
-                        const T* k, const T* v, const float* s, cudaStream_t st) {
+                        const T* k, const T* v, const float* s, bool folded, cudaStream_t st) {
   const Plan& P = h->plan;
   const PlanDev& pd = up.pd;
   ProfScope ps(h, 3, st);
-  for (size_t dpt = 0; dpt + 1 < P.depth_begin.size(); ++dpt) {
-    launch_select_resolve(g, pd, P.depth_begin[dpt], P.depth_begin[dpt + 1], L.mu, s, st);
+  if (!folded) {          // the score producer did not fold mu (injection, SIMT path)
+    launch_ema_fold(g, L.mu, s, st);
     ++h->launches;
   }
-  MaintItems it{};
-  it.items = up.maint_items;
-  it.phase = up.maint_phase;
-  it.done = L.maint_done;
-  it.ticket = L.maint_done + (size_t)(g.N + 1) * g.B * g.Hkv;
-  it.ticket_base = L.maint_tickets;
-  L.maint_tickets += (uint32_t)up.n_maint_items * (uint32_t)(g.B * g.Hkv);
-  for (int ph = 0; ph <= g.N; ++ph) {
-    L.maint_cum[ph] += (uint32_t)up.maint_per_phase[ph];
-    it.expect[ph] = L.maint_cum[ph];
+  // depth-0 selections (every selection unless m > c wraps a level inside the chunk) are
+  // resolved inside the maintenance block that moves their winner; deeper ones beforehand
+  const bool deep = P.depth_begin.size() > 2;
+  if (deep) {
+    for (size_t dpt = 0; dpt + 1 < P.depth_begin.size(); ++dpt) {
+      launch_select_resolve(g, pd, P.depth_begin[dpt], P.depth_begin[dpt + 1], L.mu, s, st);
+      ++h->launches;
+    }
   }
-  StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin};
-  launch_maint<T>(g, pd, it, up.n_maint_items, sd, k, v, s, st);
-  ++h->launches;
-  // algorithmic bytes: EMA 20 B per resident (mu r/w + s), each final row write moves
-  // K, V, mu, origin once (read + write)
+  MaintItems it{};
+  it.inline_sel = deep ? 0 : 1;
+  it.moved = maint_moved_ptr(h, L);
+  it.rec = up.maint_rec;
+  it.chunk = up.maint_chunk;
+  it.n_chunk = up.n_maint_chunk;
+  it.ticket = L.maint_ctl;
+  it.flags = L.maint_ctl + maint_ctl_head((size_t)g.B * g.Hkv);
+  it.ticket_base = L.maint_tickets;             // every (b, g) ticket advances by n_items
+  L.maint_tickets += (uint32_t)up.n_maint_items;
+  if (++L.maint_epoch == 0) L.maint_epoch = 1;
+  it.epoch = L.maint_epoch;
+  StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin, k, v};
+  launch_maint<T>(g, pd, it, up.n_maint_items, sd, s, st);
+  h->launches += (up.n_maint_items > 0 ? 1 : 0) + (up.n_maint_chunk > 0 ? 1 : 0);
+  h->moved_chunk += (uint64_t)up.n_maint_chunk * g.B * g.Hkv;
+  // algorithmic bytes: EMA 20 B per resident (mu r/w + s) when folded here; each row actually
+  // rewritten moves K, V, mu, origin once (read + write): counted on the device (it.moved) and
+  // added by cascade_profile_read
   const double bg = (double)g.B * g.Hkv;
-  const double row = 2.0 * (2.0 * g.d * sizeof(T) + 16.0);
-  ps.finish(bg * (20.0 * g.n_cached + row * (double)(P.mov.size() / 2)));
+  ps.finish(folded ? 0.0 : bg * 20.0 * g.n_cached);
 }
 
 template <typename T>
@@ -593,6 +675,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     tp.scale_log2 = g.scale_log2;
     tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
     tp.q_rot = q_rot; tp.k_rot = k_rot; tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
+    tp.mu = L.mu; tp.decay = g.decay;   // pass 2 folds the EMA in its epilogue
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);
@@ -617,7 +700,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     }
   }
   h->launches += 3;
-  launch_maintenance<T>(h, g, L, up, k, v, L.s, st);
+  launch_maintenance<T>(h, g, L, up, k, v, L.s, /*folded=*/std::is_same<T, __nv_bfloat16>::value, st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;   // commit the mirror
   h->m_last[layer] = m;
@@ -740,9 +823,10 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   const PlanDev& pd = up.pd;
   if (h->cfg.dtype == CASCADE_BF16)
     launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
-                                      static_cast<const __nv_bfloat16*>(v), s, st);
+                                      static_cast<const __nv_bfloat16*>(v), s, false, st);
   else
-    launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k), static_cast<const float*>(v), s, st);
+    launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k), static_cast<const float*>(v), s, false,
+                              st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;
   h->m_last[layer] = 0;
@@ -768,9 +852,9 @@ cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
       cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess ||
-      cudaMemsetAsync(L.maint_done, 0, h->sz.maint_done, st) != cudaSuccess)
+      cudaMemsetAsync(L.maint_ctl, 0, 4 * (size_t)h->cfg.batch * h->cfg.num_kv_heads, st) !=
+          cudaSuccess)   // the tickets; flags and the moved-row count keep running
     return CASCADE_ERR_CUDA;
-  std::memset(L.maint_cum, 0, sizeof(L.maint_cum));
   L.maint_tickets = 0;
   h->mirrors[layer] = cascade_mirror{};
   h->m_last[layer] = 0;
@@ -780,6 +864,8 @@ cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
 cascade_status cascade_profile_enable(cascade_handle* h, int32_t enable) {
   if (!h) return CASCADE_ERR_INVALID_ARG;
   h->profiling = enable != 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return CASCADE_ERR_CUDA;
+  h->moved_seen = moved_total(h);
   return CASCADE_OK;
 }
 
@@ -796,6 +882,12 @@ cascade_status cascade_profile_read(cascade_handle* h, double* ms, int64_t* coun
     }
     h->recs[c].clear();
   }
+  // maintenance rows actually rewritten since the last read: K, V (d elements each), mu and
+  // origin (8 B each), read once and written once
+  const uint64_t now = moved_total(h);
+  const double row = 2.0 * (2.0 * h->cfg.head_dim * (double)elem_size(h->cfg.dtype) + 16.0);
+  work[3] += row * (double)(now - h->moved_seen);
+  h->moved_seen = now;
   return CASCADE_OK;
 }
 

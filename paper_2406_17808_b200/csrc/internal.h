@@ -63,6 +63,8 @@ struct StateDev {
   T* v;            // [B*Hkv][S_tot][d]
   double* mu;      // [B*Hkv][S_tot]
   int64_t* origin; // [B*Hkv][S_tot]
+  const T* k_in;   // [B][m][Hkv][d] this chunk's keys (pre-RoPE) and values (maintenance sources)
+  const T* v_in;
 };
 
 // ---- launchers (defined in the .cu files) --------------------------------
@@ -82,22 +84,32 @@ void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, c
 void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end,
                            const double* mu, const float* s, cudaStream_t st);
 
-// One maintenance launch per chunk (k_maint.cu): items = (phase, slice) in phase order.
-constexpr int kMaintSlots = 512;   // slots folded per maintenance block (2 per thread)
-constexpr int kMaintMoves = 32;    // rows written per maintenance block (4 per warp)
+// One maintenance launch per chunk (k_maint.cu): a block per (item, b*g).
+constexpr int kMaintMoves = 64;    // moves per item (8 per warp), all reading a resident slot
 struct MaintItems {
-  const int4* items;          // [n_items] slot_lo, slot_len, move_begin, move_end (phase-major)
-  const int32_t* phase;       // [n_items] 0 .. N-1 = C_N .. C_1, N = sinks
-  uint32_t* done;             // [(N+1) * B*Hkv] cumulative completed blocks per (phase, b*g), wrapping
+  // [n_items][1 + kMaintMoves] int4: header {n_moves, dep_lo, dep_hi, phase}, then per move
+  // {dst, ref, cand, inc} (cand/inc: the selection's operands when ref < 0).  Items
+  // [dep_lo, dep_hi) read this item's destinations; they are all earlier items.
+  const int4* rec;
+  uint32_t* flags;            // [max_items][B*Hkv] epoch of the last launch whose item loaded
   uint32_t* ticket;           // block start order (blocks only wait on blocks that started earlier)
+  unsigned long long* moved;  // [B*Hkv] rows rewritten by maint_kernel (selection outcomes), byte count
   uint32_t ticket_base;       // ticket value of this launch's first block
-  uint32_t expect[CASCADE_MAX_LEVELS + 1];   // done[p] once phase p of this chunk is complete
+  uint32_t epoch;             // this launch's flag value (never 0)
+  int32_t inline_sel;         // 1: every selection is depth 0, resolved in the block that moves it
+  const int4* chunk;          // [n_chunk] {dst, ref, cand, inc}: moves that read no resident slot
+  int32_t n_chunk;
 };
 template <typename T>
 void launch_maint(const Geometry& g, const PlanDev& p, const MaintItems& it, int n_items, StateDev<T> sd,
-                  const T* k_in, const T* v_in, const float* s, cudaStream_t st);
+                  const float* s, cudaStream_t st);
 
 void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
+
+// EMA fold of every pre-chunk resident, mu <- decay*mu + s (Q4), for the paths whose
+// score producer does not fold (score injection, the SIMT fp32 path); the tcgen05 pass 2
+// folds in its epilogue.
+void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t st);
 
 // tcgen05 attention (k_attn_tc.cu)
 struct TcParams {
@@ -113,6 +125,8 @@ struct TcParams {
                                 //             minus the EMA row weight (+inf past m)
   const float* log2w;           // [m]  log2 of the EMA row weights
   float* s;                     // [B*Hkv][S_tot + m]
+  double* mu;                   // [B*Hkv][S_tot] EMA state: pass 2 folds mu <- decay*mu + s
+  double decay;                 // gamma^m
 };
 // single-token decode (k_decode.cu)
 struct DecodeParams {

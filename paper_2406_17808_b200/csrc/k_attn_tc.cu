@@ -331,6 +331,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   uint64_t* s_full = bars + 9;                 // [2]
   uint64_t* s_free = bars + 11;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  double* smu = reinterpret_cast<double*>(bars + 14);   // [2][128] EMA operands of the two key tiles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bgi = blockIdx.y;
@@ -415,6 +416,16 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         tc::mma_commit(q_empty + st);
       }
     }
+  } else if (warp == 3) {
+    // EMA operands (mu) of the resident key tiles, staged for the epilogue's fold so the
+    // math warps neither wait on HBM at the end nor hold them in registers
+    if (resident) {
+      for (int w = 0; w < n_here; ++w) {
+        const int2 tl = p.res_tiles[first + w];
+        for (int j = lane; j < tl.y; j += 32) smu[w * 128 + j] = p.mu[bg * p.S_tot + tl.x + j];
+      }
+    }
+    tc::named_bar_sync(1, 544);
   } else if (warp >= 4) {
     const int wgi = (warp - 4) >> 2;                      // 0..3
     const int wg = wgi & 1, half = wgi >> 1;              // key tile of the pair, column half
@@ -459,13 +470,15 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
       }
     }
-    tc::named_bar_sync(1, 512);                           // all halves' per-head sums in smem
+    tc::named_bar_sync(1, 544);                           // all halves' per-head sums in smem
     if (half == 0 && active && r < klen) {
       const float* h0 = sacc + (wg * 2 + 0) * p.G * 128;
       const float* h1 = sacc + (wg * 2 + 1) * p.G * 128;
       float best = 0.f;
       for (int hh = 0; hh < p.G; ++hh) best = fmaxf(best, h0[hh * 128 + r] + h1[hh * 128 + r]);
       p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
+      if (resident)                                       // EMA fold (Q4), never an FMA
+        p.mu[bg * p.S_tot + kstart + r] = __dadd_rn(__dmul_rn(p.decay, smu[wg * 128 + r]), (double)best);
     }
   }
   tc::tc_fence_before();
@@ -482,7 +495,8 @@ size_t attn_fwd_tc_smem(int d) {
 }
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
-  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + (size_t)4 * G * 128 * 4 + 16 * 8 + 64;
+  return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + (size_t)4 * G * 128 * 4 + 16 * 8 + 64 +
+         2 * 128 * 8;
 }
 
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,

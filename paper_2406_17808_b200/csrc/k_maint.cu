@@ -5,36 +5,66 @@
 // the counters, never on mu or on the head (the host plan simulates it, plan.cpp).
 // What depends on mu is the outcome of each selection.  The device work is:
 //
-// The EMA fold (P:154 over m rows, Q4) is mu <- g*mu + s in IEEE double (__dmul_rn/__dadd_rn,
-// never contracted into an FMA); semantically every fold precedes every insertion (Q9).  Since
-// the fold is a pure function of the pre-chunk (mu, s), it is evaluated where it is needed:
-//  1. select_resolve: winner of selection k = cand if fold(cand) > fold(inc) else inc
-//                (strict '>'), per (b, g), folding both operands on the fly.  Operands
-//                that are themselves winners of earlier selections are resolved in
-//                dependency-depth order (one launch per depth; depth 0 covers every config).
-//  2. maint:     ONE launch: a block per (item, b*g); an item is a range of one phase's slots
-//                plus the moves landing in it.  Phases run C_N, ..., C_1, then the sinks.  A
-//                block folds the residents of its range in place and writes the range's final
-//                occupants (K_raw, V, mu = fold(source), origin).  A slot of C_i only receives
-//                tokens from C_{<i} or the chunk, so a block of phase p stores only after every
-//                block of phase p-1 is done (device-scope counter per (phase, b*g)) -- those
-//                read the slots phase p overwrites -- and its sources are still unfolded,
-//                pre-chunk rows, which it loads before waiting.
+//  0. EMA fold (P:154 over m rows, Q4): mu <- g*mu + s in IEEE double (__dmul_rn/__dadd_rn,
+//     never contracted into an FMA), before any insertion (Q9).  The tcgen05 pass 2 does it in
+//     its epilogue; ema_fold_kernel serves score injection and the SIMT path.
+//  1. select_resolve (only when a selection operand is itself a selection of the same chunk,
+//     i.e. m > c wraps a level): winner = cand if mu(cand) > mu(inc) else inc (strict '>',
+//     P:615), per (b, g), one launch per dependency depth.  Depth-0 selections -- all of them
+//     in every benchmark config -- are resolved inside the block that moves the winner.
+//  2. maint: ONE launch, a block per (item, b*g).  An item is a run of <= 64 moves of one
+//     phase (phases C_N, ..., C_1, sinks; destinations sorted), with at most kMaintStaged
+//     moves that read a resident slot.  Hazard: a move's source may be a pre-chunk slot that
+//     another item overwrites (an evictee carried to the next sub-cache).  The host
+//     lists, per item, the items that READ its destinations (always earlier items, deeper
+//     sub-caches); a block loads resident sources into shared memory (cp.async), publishes
+//     "loaded" (a per-(item, b*g) epoch flag), waits only for the flags of its readers, then
+//     stores.  Chunk-row sources are never overwritten: copied after the wait, straight
+//     through registers.
 //
-// All HBM-bound: coalesced 16-byte vector copies, a full warp per moved (K | V) row pair.
+// All HBM-bound: coalesced 16-byte vectors, a full warp per moved (K | V) row pair.
 #include "common.cuh"
 
 namespace cascade {
+
+__device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 
 __device__ __forceinline__ int32_t resolve_ref(int32_t ref, const int32_t* __restrict__ res) {
   return ref >= 0 ? ref : res[-ref - 1];
 }
 
-// mu of a concrete source after the fold: g*mu + s of a pre-chunk slot (read unfolded), or s of
-// a chunk row (mu starts at 0).
+// mu of a concrete source after the fold: the folded mu of a pre-chunk slot, or s of a chunk
+// row (mu starts at 0).
 __device__ __forceinline__ double src_mu(const Geometry& g, int32_t x, const double* mu_bg,
                                          const float* s_bg) {
-  return x < g.S_tot ? __dadd_rn(__dmul_rn(g.decay, mu_bg[x]), (double)s_bg[x]) : (double)s_bg[x];
+  return x < g.S_tot ? mu_bg[x] : (double)s_bg[x];
+}
+
+__global__ void ema_fold_kernel(Geometry g, double* __restrict__ mu, const float* __restrict__ s) {
+  const int BG = g.B * g.Hkv;
+  const long long total = (long long)BG * g.S_tot;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long bg = i / g.S_tot;
+    const int x = (int)(i - bg * g.S_tot);
+    bool valid = x < g.sink_pre;
+    if (x >= g.alpha) {
+      const int lvl = (x - g.alpha) / g.c;
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < CASCADE_MAX_LEVELS; ++k) cnt = k == lvl ? g.counts_pre[k] : cnt;
+      valid = x - g.alpha - lvl * g.c < cnt;
+    }
+    if (valid) mu[i] = __dadd_rn(__dmul_rn(g.decay, mu[i]), (double)s[bg * (g.S_tot + g.m) + x]);
+  }
+}
+
+void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t st) {
+  const long long total = (long long)g.B * g.Hkv * g.S_tot;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+  ema_fold_kernel<<<blocks, 256, 0, st>>>(g, mu, s);
 }
 
 __global__ void select_resolve_kernel(Geometry g, PlanDev p, int32_t begin, int32_t end,
@@ -63,135 +93,214 @@ void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, i
   select_resolve_kernel<<<blocks, 256, 0, st>>>(g, p, begin, end, mu, s);
 }
 
-// One block = one item (a range of <= kMaintSlots slots of one phase, with the <= kMaintMoves
-// moves whose destination falls in it) for one (b, g).  Every load (fold operands, source rows)
-// is issued before the wait: a block's reads only touch slots of shallower levels and the chunk,
-// which no block overwrites before this one publishes.  Only the stores wait for phase p-1.
-template <typename T, int VPL>
-__global__ void __launch_bounds__(256) maint_kernel(Geometry g, PlanDev p, MaintItems it, StateDev<T> sd,
-                                                    const T* __restrict__ k_in, const T* __restrict__ v_in,
-                                                    const float* __restrict__ s) {
-  __shared__ uint32_t s_ticket;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(it.ticket, 1u);
-  __syncthreads();
+// maint_kernel: one block (8 warps) = one item for one (b, g).  Warp w owns moves 8w .. 8w+7 of
+// the item; lane j < 8 resolves move j (source, destination, mu, origin stay in its registers).
+// Every move of an item reads a resident slot; all rows go to shared memory before publishing.
+template <typename T>
+__global__ void __launch_bounds__(256, 6) maint_kernel(Geometry g, PlanDev p, MaintItems it, StateDev<T> sd,
+                                                       const float* __restrict__ s) {
+  constexpr int kPerWarp = kMaintMoves / 8;
+  extern __shared__ __align__(16) int4 s_rows[];          // [kMaintMoves][2 * nvec]
+  __shared__ uint32_t s_ticket, s_moved;
   const int BG = g.B * g.Hkv;
-  const uint32_t logical = s_ticket - it.ticket_base;     // start order, not blockIdx: no deadlock
-  const int item = (int)(logical / BG), bg = (int)(logical - (uint32_t)item * BG);
-  const int4 d = it.items[item];                           // slot_lo, slot_len, move_begin, move_end
-  const int phase = it.phase[item];
+  const int bg = (int)(blockIdx.x % (unsigned)BG);
+  // per-(b, g) start-order ticket: a block only waits on items of its (b, g) that started before it
+  if (threadIdx.x == 0) { s_ticket = atomicAdd(it.ticket + bg, 1u); s_moved = 0; }
+  __syncthreads();
+  const int item = (int)(s_ticket - it.ticket_base);
+  const int4* rec = it.rec + (size_t)item * (1 + kMaintMoves);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = warp * kPerWarp + lane;
+  // header and this lane's move record load together (records are padded to kMaintMoves)
+  const int4 hd = rec[0];                                  // n_moves, dep_lo, dep_hi, phase
+  const int4 mv = rec[1 + (lane < kPerWarp ? e : 0)];     // dst, ref, cand, inc
   const long long sbase = (long long)bg * g.S_tot;
-  double* mu = sd.mu + sbase;
+  const double* mu = sd.mu + sbase;
   const float* s_bg = s + (long long)bg * (g.S_tot + g.m);
-
-  // fold operands of the slice's pre-chunk residents
-  const int lvl = phase < g.N ? g.N - 1 - phase : -1;    // 0-based sub-cache, -1 = sinks
-  const int valid_end = min(d.x + d.y, lvl < 0 ? g.sink_pre : g.alpha + lvl * g.c + g.counts_pre[lvl]);
-  double f[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int x = d.x + threadIdx.x + j * 256;
-    if (x < valid_end) f[j] = __dadd_rn(__dmul_rn(g.decay, mu[x]), (double)s_bg[x]);
-  }
-  // source rows of the moves: warp w takes moves d.z + w + 8 j; lane l carries 16-byte vectors
-  // l, l + 32, ... of the (K | V) row pair
   const int nvec = g.d * (int)sizeof(T) / 16;             // vectors per K (or V) row
-  const int gg = bg % g.Hkv, b = bg / g.Hkv;
-  const int32_t* res = p.resolved + (long long)bg * p.sel_cap;
-  int32_t dst[4];
-  int4 buf[4][VPL];
-  double mu_new[4];
-  int64_t org[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int e = d.z + warp + 8 * j;
-    dst[j] = -1;
-    if (e < d.w) {
-      const int32_t dd = p.mov[2 * e];
-      const int32_t src = resolve_ref(p.mov[2 * e + 1], res);
-      if (src != dd) {                                     // resident won its selection: stays
-        dst[j] = dd;
-        const T *ks, *vs;
-        if (src < g.S_tot) {
-          ks = sd.k_raw + (sbase + src) * g.d;
-          vs = sd.v + (sbase + src) * g.d;
-          mu_new[j] = __dadd_rn(__dmul_rn(g.decay, mu[src]), (double)s_bg[src]);  // still unfolded
-          org[j] = sd.origin[sbase + src];
-        } else {
-          const int r = src - g.S_tot;
-          ks = k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-          vs = v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-          mu_new[j] = (double)s_bg[src];
-          org[j] = g.t0 + r;
-        }
-#pragma unroll
-        for (int u = 0; u < VPL; ++u) {
-          const int i = lane + 32 * u;
-          if (i < nvec) buf[j][u] = __ldcs(reinterpret_cast<const int4*>(ks) + i);
-          else if (i < 2 * nvec) buf[j][u] = __ldcs(reinterpret_cast<const int4*>(vs) + i - nvec);
-        }
+
+  int32_t my_dst = -1, my_src = 0;
+  double my_mu = 0.0;
+  int64_t my_org = 0;
+  if (lane < kPerWarp && e < hd.x) {
+    int32_t src = mv.y;
+    if (src < 0) {
+      if (it.inline_sel) {
+        // winner of a depth-0 selection: cand if mu(cand) > mu(inc), strict (Q2); both
+        // operands' mu and origin are loaded together
+        const double mc = src_mu(g, mv.z, mu, s_bg), mi = src_mu(g, mv.w, mu, s_bg);
+        const int64_t oc = mv.z < g.S_tot ? sd.origin[sbase + mv.z] : g.t0 + (mv.z - g.S_tot);
+        const int64_t oi = mv.w < g.S_tot ? sd.origin[sbase + mv.w] : g.t0 + (mv.w - g.S_tot);
+        const bool cw = mc > mi;
+        src = cw ? mv.z : mv.w;
+        my_mu = cw ? mc : mi;
+        my_org = cw ? oc : oi;
+      } else {
+        src = p.resolved[(long long)bg * p.sel_cap + (-src - 1)];
+        my_mu = src_mu(g, src, mu, s_bg);
+        my_org = src < g.S_tot ? sd.origin[sbase + src] : g.t0 + (src - g.S_tot);
       }
+    } else {
+      my_mu = src_mu(g, src, mu, s_bg);                    // folded (Q9) or a new token's s
+      my_org = src < g.S_tot ? sd.origin[sbase + src] : g.t0 + (src - g.S_tot);
+    }
+    if (src != mv.x) {                                     // resident won its selection: stays
+      my_dst = mv.x;
+      my_src = src;
     }
   }
-  // wait until every block of phase p-1 of this (b, g) is done: they read the slots we overwrite
-  if (phase > 0 && phase < g.N) {
-    if (threadIdx.x == 0) {
-      const uint32_t* ctr = it.done + (phase - 1) * BG + bg;
-      const uint32_t want = it.expect[phase - 1];
+  const uint32_t any = __ballot_sync(0xffffffffu, my_dst >= 0);
+  const int gg = bg % g.Hkv, b = bg / g.Hkv;
+#pragma unroll
+  for (int j = 0; j < kPerWarp; ++j) {
+    const int32_t sj = __shfl_sync(0xffffffffu, my_src, j);
+    if (!((any >> j) & 1u)) continue;
+    const T *ks, *vs;
+    if (sj < g.S_tot) {
+      ks = sd.k_raw + (sbase + sj) * g.d;
+      vs = sd.v + (sbase + sj) * g.d;
+    } else {                                               // a selection won by a chunk row
+      const int r = sj - g.S_tot;
+      ks = sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
+      vs = sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
+    }
+    int4* row = s_rows + (warp * kPerWarp + j) * 2 * nvec;
+    for (int i = lane; i < 2 * nvec; i += 32) {
+      const int4* gsrc = i < nvec ? reinterpret_cast<const int4*>(ks) + i
+                                  : reinterpret_cast<const int4*>(vs) + (i - nvec);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc_smem_u32(row + i)), "l"(gsrc)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  // every loaded value must have ARRIVED before this block publishes, or a store of a later
+  // item could overtake a load still in flight.  The rows are in shared memory (waited above);
+  // the register operands are folded into one word that feeds the barrier's predicate
+  // (consuming a register waits for its load).
+  const uint32_t sink = (uint32_t)__double2loint(my_mu) ^ (uint32_t)my_org;
+  __syncthreads_or(sink == 0x9E3779B9u);
+  if (warp == 0) {
+    if (lane == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(it.flags + (size_t)item * BG + bg), "r"(it.epoch)
+                   : "memory");
+    }
+    // wait for the items that read this item's destinations (host-computed, all earlier)
+    for (int j = hd.y + lane; j < hd.z; j += 32) {
+      const uint32_t* f = it.flags + (size_t)j * BG + bg;
       uint32_t v;
       while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-        if ((int32_t)(v - want) >= 0) break;
-        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v == it.epoch) break;
+        __nanosleep(20);
       }
     }
   }
   __syncthreads();
+  if (lane == 0 && any) atomicAdd(&s_moved, (uint32_t)__popc(any));
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int x = d.x + threadIdx.x + j * 256;
-    if (x < valid_end) mu[x] = f[j];
+  for (int j = 0; j < kPerWarp; ++j) {
+    const int32_t dj = __shfl_sync(0xffffffffu, my_dst, j);
+    if (!((any >> j) & 1u)) continue;
+    T* kd = sd.k_raw + (sbase + dj) * g.d;
+    T* vd = sd.v + (sbase + dj) * g.d;
+    const int4* row = s_rows + (warp * kPerWarp + j) * 2 * nvec;
+    for (int i = lane; i < 2 * nvec; i += 32) {
+      if (i < nvec) __stcs(reinterpret_cast<int4*>(kd) + i, row[i]);
+      else __stcs(reinterpret_cast<int4*>(vd) + i - nvec, row[i]);
+    }
   }
-  __syncthreads();                                         // moves overwrite folded slots' mu
+  if (my_dst >= 0) {
+    sd.mu[sbase + my_dst] = my_mu;
+    sd.origin[sbase + my_dst] = my_org;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_moved) atomicAdd(it.moved + bg, (unsigned long long)s_moved);
+}
+
+// chunk_moves_kernel: moves that read no resident slot (chunk tokens entering C_1 or the sinks;
+// selections between two chunk rows).  Launched after maint_kernel, so every resident read of
+// the chunk is done; no ordering among them.  One warp per kChunkPerWarp (move, b*g) pairs, all
+// loads in flight before the stores.
+constexpr int kChunkPerWarp = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) chunk_moves_kernel(Geometry g, PlanDev p, MaintItems it, StateDev<T> sd,
+                                                          const float* __restrict__ s) {
+  const int BG = g.B * g.Hkv;
+  const int lane = threadIdx.x & 31;
+  const int bg = blockIdx.y;
+  const int w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kChunkPerWarp;
+  const float* s_bg = s + (long long)bg * (g.S_tot + g.m);
+  const long long sbase = (long long)bg * g.S_tot;
+  const int gg = bg % g.Hkv, b = bg / g.Hkv;
+  const int nvec = g.d * (int)sizeof(T) / 16;
+  int4 buf[kChunkPerWarp][2];
+  int32_t dst[kChunkPerWarp], src[kChunkPerWarp];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (dst[j] < 0) continue;
-    T* kd = sd.k_raw + (sbase + dst[j]) * g.d;
-    T* vd = sd.v + (sbase + dst[j]) * g.d;
+  for (int u = 0; u < kChunkPerWarp; ++u) {
+    const int e = w0 + u;
+    dst[u] = -1;
+    if (e >= it.n_chunk) continue;
+    const int4 mv = it.chunk[e];                           // dst, ref, cand, inc
+    int32_t sr = mv.y;
+    if (sr < 0) {
+      sr = it.inline_sel ? ((double)s_bg[mv.z] > (double)s_bg[mv.w] ? mv.z : mv.w)   // P:615, strict
+                         : p.resolved[(long long)bg * p.sel_cap + (-sr - 1)];
+    }
+    dst[u] = mv.x; src[u] = sr;
+    const int r = sr - g.S_tot;
+    const int4* ks = reinterpret_cast<const int4*>(sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
+    const int4* vs = reinterpret_cast<const int4*>(sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
 #pragma unroll
-    for (int u = 0; u < VPL; ++u) {
-      const int i = lane + 32 * u;
-      if (i < nvec) reinterpret_cast<int4*>(kd)[i] = buf[j][u];
-      else if (i < 2 * nvec) reinterpret_cast<int4*>(vd)[i - nvec] = buf[j][u];
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      if (i < nvec) buf[u][h] = __ldcs(ks + i);
+      else if (i < 2 * nvec) buf[u][h] = __ldcs(vs + i - nvec);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kChunkPerWarp; ++u) {
+    if (dst[u] < 0) continue;
+    int4* kd = reinterpret_cast<int4*>(sd.k_raw + (sbase + dst[u]) * g.d);
+    int4* vd = reinterpret_cast<int4*>(sd.v + (sbase + dst[u]) * g.d);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      if (i < nvec) __stcs(kd + i, buf[u][h]);
+      else if (i < 2 * nvec) __stcs(vd + i - nvec, buf[u][h]);
     }
     if (lane == 0) {
-      mu[dst[j]] = mu_new[j];
-      sd.origin[sbase + dst[j]] = org[j];
+      sd.mu[sbase + dst[u]] = (double)s_bg[src[u]];        // new token: mu = s
+      sd.origin[sbase + dst[u]] = g.t0 + (src[u] - g.S_tot);
     }
-  }
-  // publish completion of this block for the next phase
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(it.done + phase * BG + bg, 1u);
   }
 }
 
 template <typename T>
 void launch_maint(const Geometry& g, const PlanDev& p, const MaintItems& it, int n_items, StateDev<T> sd,
-                  const T* k_in, const T* v_in, const float* s, cudaStream_t st) {
-  if (n_items <= 0) return;
-  const int vpl = (2 * g.d * (int)sizeof(T) / 16 + 31) / 32;
-  const int blocks = n_items * g.B * g.Hkv;
-  if (vpl <= 1) maint_kernel<T, 1><<<blocks, 256, 0, st>>>(g, p, it, sd, k_in, v_in, s);
-  else maint_kernel<T, 2><<<blocks, 256, 0, st>>>(g, p, it, sd, k_in, v_in, s);
+                  const float* s, cudaStream_t st) {
+  const int BG = g.B * g.Hkv;
+  if (n_items > 0) {
+    const size_t smem = (size_t)kMaintMoves * 2 * g.d * sizeof(T);
+    static bool attr_set[2] = {false, false};
+    bool& done = attr_set[sizeof(T) == 2];
+    if (!done) {   // full shared-memory carveout: 6 blocks of 32 KB per SM
+      cudaFuncSetAttribute(maint_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(maint_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      done = true;
+    }
+    maint_kernel<T><<<n_items * BG, 256, smem, st>>>(g, p, it, sd, s);
+  }
+  if (it.n_chunk > 0) {
+    const int warps = (it.n_chunk + kChunkPerWarp - 1) / kChunkPerWarp;
+    chunk_moves_kernel<T><<<dim3((warps + 7) / 8, BG), 256, 0, st>>>(g, p, it, sd, s);
+  }
 }
 
 template void launch_maint<float>(const Geometry&, const PlanDev&, const MaintItems&, int, StateDev<float>,
-                                  const float*, const float*, const float*, cudaStream_t);
+                                  const float*, cudaStream_t);
 template void launch_maint<__nv_bfloat16>(const Geometry&, const PlanDev&, const MaintItems&, int,
-                                          StateDev<__nv_bfloat16>, const __nv_bfloat16*, const __nv_bfloat16*,
-                                          const float*, cudaStream_t);
+                                          StateDev<__nv_bfloat16>, const float*, cudaStream_t);
 
 __global__ void positions_kernel(Geometry g, int32_t* __restrict__ pe) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.S_tot; x += gridDim.x * blockDim.x)
