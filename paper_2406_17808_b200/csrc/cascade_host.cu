@@ -24,11 +24,7 @@ constexpr int kRing = 8;   // pinned schedule staging buffers in flight
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-// maintenance items per chunk: every item but the last of a phase holds kMaintMoves moves,
-// and a chunk of M tokens touches <= 2 (N + 1) M slots
-int32_t max_maint_items(int32_t N, int32_t M) { return 2 * (N + 1) * M / kMaintMoves + N + 2; }
-// words of maint_ctl before the flags: one ticket per (b, g) (padded to even), the moved count
-size_t maint_ctl_head(size_t BG) { return ((BG + 1) & ~size_t(1)) + 2 * BG; }
+
 
 size_t elem_size(int32_t dtype) { return dtype == CASCADE_BF16 ? 2 : 4; }
 
@@ -39,10 +35,9 @@ struct LayerBufs {
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
   float* dec_logits; float* dec_part_o; float* dec_part_ml;
-  uint32_t* maint_ctl;      // per-(b, g) block tickets, the 64-bit count of rows actually
-                            // rewritten, then per-(item, b*g) epoch flags (MaintItems)
-  uint32_t maint_tickets;   // host copy: maintenance blocks launched (wrapping)
-  uint32_t maint_epoch;     // host copy: epoch of the last maintenance launch (never 0)
+  uint32_t* maint_ctl;      // [0] grid-barrier counter, then per-(b, g) 64-bit counts of rows
+                            // actually rewritten (8-byte aligned)
+  uint32_t maint_barrier;   // host copy of the barrier counter (wrapping)
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
   CUtensorMap tm_kraw;                    // TMA map of the pre-RoPE key state (decode)
 };
@@ -103,7 +98,7 @@ Sizes compute_sizes(const cascade_config& c) {
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
-                          4 * (1 + kMaintMoves) * max_maint_items(N, M) + 4 * 2 * (N + 1) * M + 48);
+                          4 * 2 * (N + 1) * M + 48);   // + maintenance moves (4 ints each, <= 2 (N+1) M)
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -122,7 +117,7 @@ Sizes compute_sizes(const cascade_config& c) {
     z.dec_part_o = align_up(bgs * ns * G * d * 4);
     z.dec_part_ml = align_up(bgs * ns * G * 2 * 4);
   }
-  z.maint_ctl = align_up(4 * maint_ctl_head(B * Hk) + (size_t)max_maint_items(N, M) * B * Hk * 4);
+  z.maint_ctl = align_up(8 + 8 * B * Hk);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
                 z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_ctl;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
@@ -163,13 +158,9 @@ struct cascade_handle {
   std::vector<cudaEvent_t> ev_pool;
   uint64_t moved_seen;      // sum over layers of the device moved-row counters at the last read
   uint64_t moved_chunk;     // chunk-row moves launched (each always rewrites its row)
-  // maintenance planning scratch: writer item of each destination slot of the current chunk
-  std::vector<int32_t> wr_item;
-  std::vector<uint32_t> wr_stamp;
-  uint32_t wr_cur;
+  // maintenance planning scratch
   std::vector<int32_t> maint_reads;
-  std::vector<int4> maint_chunk;
-  bool maint_split;         // chunk-row moves in their own launch (CASCADE_MAINT_SPLIT, default 0)
+  std::vector<int4> maint_staged, maint_chunk;
 };
 
 namespace {
@@ -291,14 +282,10 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->c = cfg->cache_size / cfg->num_cascades;
   h->S_tot = h->alpha + cfg->cache_size;
   h->planner.configure(h->alpha, h->N, h->c);
-  h->wr_item.assign(h->S_tot, 0);
-  h->wr_stamp.assign(h->S_tot, 0u);
-  h->wr_cur = 0;
   h->launches = 0;
   h->ring_pos = 0;
   h->profiling = false;
   h->moved_seen = 0;
-  { const char* e = std::getenv("CASCADE_MAINT_SPLIT"); h->maint_split = e && std::atoi(e) != 0; }
   h->moved_chunk = 0;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
 
@@ -319,8 +306,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.dec_part_o = reinterpret_cast<float*>(take(sz.dec_part_o));
     L.dec_part_ml = reinterpret_cast<float*>(take(sz.dec_part_ml));
     L.maint_ctl = reinterpret_cast<uint32_t*>(take(sz.maint_ctl));
-    L.maint_tickets = 0;
-    L.maint_epoch = 0;
+    L.maint_barrier = 0;
   }
   h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
@@ -426,8 +412,8 @@ struct Upload {
   const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
   const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
   int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
-  const int4* maint_rec;       // maintenance item records (MaintItems::rec)
-  int32_t n_maint_items;
+  const int4* maint_staged;    // moves that read a resident slot (MaintItems::staged)
+  int32_t n_maint_staged;
   const int4* maint_chunk;     // moves that read no resident slot (MaintItems::chunk)
   int32_t n_maint_chunk;
 };
@@ -498,68 +484,31 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
       }
     }
   }
-  // maintenance items, phase by phase (C_N .. C_1, sinks): runs of <= kMaintMoves of the
-  // phase's moves (sorted by destination) of which <= kMaintStaged read a resident slot
+  // maintenance moves, in phase order (C_N .. C_1, sinks): those that read a resident slot
+  // (evictees, selections) and those that read only chunk rows
   const size_t mi_off = pad4(dt_off + 4 * (size_t)ndt);
-  int4* rec = reinterpret_cast<int4*>(buf + mi_off);
-  int32_t nmi = 0;
   const int32_t S_tot = h->S_tot;
-  // concrete slots a plan reference reads (a selection reads both operands)
   std::vector<int32_t>& rd = h->maint_reads;
-  auto reads = [&](int32_t ref, auto&& self) -> void {
+  auto reads = [&](int32_t ref, auto&& self) -> void {    // concrete slots a reference reads
     if (ref >= 0) { if (ref < S_tot) rd.push_back(ref); return; }
     const int32_t k = -ref - 1;
     self(P.sel[3 * k + 1], self);
     self(P.sel[3 * k + 2], self);
   };
-  if (++h->wr_cur == 0) { std::fill(h->wr_stamp.begin(), h->wr_stamp.end(), 0u); h->wr_cur = 1; }
+  std::vector<int4>& staged = h->maint_staged;
   std::vector<int4>& chunk_moves = h->maint_chunk;
+  staged.clear();
   chunk_moves.clear();
-  for (int32_t ph = 0; ph <= h->N; ++ph) {
-    int32_t open = -1, n = 0;
-    for (int32_t e = P.phase_begin[ph]; e < P.phase_begin[ph + 1]; ++e) {
-      const int32_t dst = P.mov[2 * e], ref = P.mov[2 * e + 1];
-      int32_t cand = 0, inc = 0;
-      if (ref < 0) { cand = P.sel[3 * (-ref - 1) + 1]; inc = P.sel[3 * (-ref - 1) + 2]; }
-      rd.clear();
-      reads(ref, reads);
-      if (rd.empty() && h->maint_split) {     // reads no resident slot: chunk_moves_kernel
-        chunk_moves.push_back(make_int4(dst, ref, cand, inc));
-        continue;
-      }
-      if (open < 0 || n == kMaintMoves) {
-        if (open >= 0) rec[open * (1 + kMaintMoves)].x = n;
-        open = nmi++;
-        rec[open * (1 + kMaintMoves)] = make_int4(0, 0, 0, ph);
-        n = 0;
-      }
-      rec[open * (1 + kMaintMoves) + 1 + n] = make_int4(dst, ref, cand, inc);
-      ++n;
-      h->wr_stamp[dst] = h->wr_cur;
-      h->wr_item[dst] = open;
-    }
-    if (open >= 0) rec[open * (1 + kMaintMoves)].x = n;
+  for (size_t e = 0; e < P.mov.size() / 2; ++e) {
+    const int32_t dst = P.mov[2 * e], ref = P.mov[2 * e + 1];
+    int32_t cand = 0, inc = 0;
+    if (ref < 0) { cand = P.sel[3 * (-ref - 1) + 1]; inc = P.sel[3 * (-ref - 1) + 2]; }
+    rd.clear();
+    reads(ref, reads);
+    (rd.empty() ? chunk_moves : staged).push_back(make_int4(dst, ref, cand, inc));
   }
-  // hazards: item J reads slot x that item W overwrites -> W waits for J's "loaded" flag.
-  // Readers sit in deeper sub-caches, i.e. earlier items (a block only waits on blocks that
-  // started before it); anything else is a planner bug.
-  for (int32_t J = 0; J < nmi; ++J) {
-    const int4 hd = rec[J * (1 + kMaintMoves)];
-    for (int32_t j = 0; j < hd.x; ++j) {
-      rd.clear();
-      reads(rec[J * (1 + kMaintMoves) + 1 + j].y, reads);
-      for (int32_t x : rd) {
-        if (h->wr_stamp[x] != h->wr_cur) continue;
-        const int32_t W = h->wr_item[x];
-        if (W == J) continue;
-        if (W < J) return CASCADE_ERR_UNSUPPORTED;
-        int4& hw = rec[W * (1 + kMaintMoves)];
-        if (hw.y == hw.z) { hw.y = J; hw.z = J + 1; }
-        else { hw.y = std::min(hw.y, J); hw.z = std::max(hw.z, J + 1); }
-      }
-    }
-  }
-  const size_t cm_off = mi_off + 4 * (1 + kMaintMoves) * (size_t)nmi;
+  std::memcpy(buf + mi_off, staged.data(), staged.size() * sizeof(int4));
+  const size_t cm_off = mi_off + 4 * staged.size();
   std::memcpy(buf + cm_off, chunk_moves.data(), chunk_moves.size() * sizeof(int4));
   const size_t total = cm_off + 4 * chunk_moves.size();
   if (total > (size_t)h->sz.plan_ints) return CASCADE_ERR_WORKSPACE;   // capacity formula broken
@@ -579,8 +528,8 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->phase_begin = L.plan + tiles_off + 2 * nt;
   up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
   up->n_dec_tiles = ndt;
-  up->maint_rec = reinterpret_cast<const int4*>(L.plan + mi_off);
-  up->n_maint_items = nmi;
+  up->maint_staged = reinterpret_cast<const int4*>(L.plan + mi_off);
+  up->n_maint_staged = (int32_t)staged.size();
   up->maint_chunk = reinterpret_cast<const int4*>(L.plan + cm_off);
   up->n_maint_chunk = (int32_t)chunk_moves.size();
   return CASCADE_OK;
@@ -588,7 +537,8 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
 
 unsigned long long* maint_moved_ptr(cascade_handle* h, LayerBufs& L) {
   const size_t BG = (size_t)h->cfg.batch * h->cfg.num_kv_heads;
-  return reinterpret_cast<unsigned long long*>(L.maint_ctl + maint_ctl_head(BG) - 2 * BG);
+  (void)BG;
+  return reinterpret_cast<unsigned long long*>(L.maint_ctl + 2);
 }
 
 uint64_t moved_total(cascade_handle* h) {
@@ -625,18 +575,16 @@ void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
   MaintItems it{};
   it.inline_sel = deep ? 0 : 1;
   it.moved = maint_moved_ptr(h, L);
-  it.rec = up.maint_rec;
+  it.staged = up.maint_staged;
+  it.n_staged = up.n_maint_staged;
   it.chunk = up.maint_chunk;
   it.n_chunk = up.n_maint_chunk;
-  it.ticket = L.maint_ctl;
-  it.flags = L.maint_ctl + maint_ctl_head((size_t)g.B * g.Hkv);
-  it.ticket_base = L.maint_tickets;             // every (b, g) ticket advances by n_items
-  L.maint_tickets += (uint32_t)up.n_maint_items;
-  if (++L.maint_epoch == 0) L.maint_epoch = 1;
-  it.epoch = L.maint_epoch;
+  it.barrier = L.maint_ctl;
+  it.barrier_base = L.maint_barrier;
+  L.maint_barrier += (uint32_t)maint_barriers<T>(g, it);
   StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin, k, v};
-  launch_maint<T>(g, pd, it, up.n_maint_items, sd, s, st);
-  h->launches += (up.n_maint_items > 0 ? 1 : 0) + (up.n_maint_chunk > 0 ? 1 : 0);
+  launch_maint<T>(g, pd, it, sd, s, st);
+  h->launches += (up.n_maint_staged > 0 || up.n_maint_chunk > 0) ? 1 : 0;
   h->moved_chunk += (uint64_t)up.n_maint_chunk * g.B * g.Hkv;
   // algorithmic bytes: EMA 20 B per resident (mu r/w + s) when folded here; each row actually
   // rewritten moves K, V, mu, origin once (read + write): counted on the device (it.moved) and
@@ -852,10 +800,10 @@ cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
       cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess ||
-      cudaMemsetAsync(L.maint_ctl, 0, 4 * (size_t)h->cfg.batch * h->cfg.num_kv_heads, st) !=
-          cudaSuccess)   // the tickets; flags and the moved-row count keep running
+      cudaMemsetAsync(L.maint_ctl, 0, 4, st) != cudaSuccess)   // the barrier; the moved-row counts
+                                                               // keep running
     return CASCADE_ERR_CUDA;
-  L.maint_tickets = 0;
+  L.maint_barrier = 0;
   h->mirrors[layer] = cascade_mirror{};
   h->m_last[layer] = 0;
   return CASCADE_OK;

@@ -84,25 +84,25 @@ void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, c
 void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end,
                            const double* mu, const float* s, cudaStream_t st);
 
-// One maintenance launch per chunk (k_maint.cu): a block per (item, b*g).
-constexpr int kMaintMoves = 64;    // moves per item (8 per warp), all reading a resident slot
+// One cooperative maintenance launch per chunk (k_maint.cu, maint_coop_kernel).
 struct MaintItems {
-  // [n_items][1 + kMaintMoves] int4: header {n_moves, dep_lo, dep_hi, phase}, then per move
-  // {dst, ref, cand, inc} (cand/inc: the selection's operands when ref < 0).  Items
-  // [dep_lo, dep_hi) read this item's destinations; they are all earlier items.
-  const int4* rec;
-  uint32_t* flags;            // [max_items][B*Hkv] epoch of the last launch whose item loaded
-  uint32_t* ticket;           // block start order (blocks only wait on blocks that started earlier)
-  unsigned long long* moved;  // [B*Hkv] rows rewritten by maint_kernel (selection outcomes), byte count
-  uint32_t ticket_base;       // ticket value of this launch's first block
-  uint32_t epoch;             // this launch's flag value (never 0)
-  int32_t inline_sel;         // 1: every selection is depth 0, resolved in the block that moves it
-  const int4* chunk;          // [n_chunk] {dst, ref, cand, inc}: moves that read no resident slot
+  const int4* staged;         // [n_staged] {dst, ref, cand, inc}: moves reading a resident slot,
+  int32_t n_staged;           //   in phase order (C_N .. C_1, sinks); cand/inc when ref < 0
+  const int4* chunk;          // [n_chunk] moves that read only chunk rows
   int32_t n_chunk;
+  uint32_t* barrier;          // grid-barrier arrival counter (monotonic, wrapping)
+  uint32_t barrier_base;      // its value when this launch starts
+  int32_t rows_per_block;     // set by launch_maint
+  unsigned long long* moved;  // [B*Hkv] rows rewritten by staged moves (selection outcomes)
+  int32_t inline_sel;         // 1: every selection is depth 0, resolved where its winner moves
 };
+struct MaintGrid { int blocks, rows_per_block; };
 template <typename T>
-void launch_maint(const Geometry& g, const PlanDev& p, const MaintItems& it, int n_items, StateDev<T> sd,
-                  const float* s, cudaStream_t st);
+void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
+                  cudaStream_t st);
+// barrier arrivals one launch adds (the host advances barrier_base by it)
+template <typename T>
+int maint_barriers(const Geometry& g, const MaintItems& it);
 
 void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
 

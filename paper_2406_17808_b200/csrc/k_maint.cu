@@ -24,6 +24,11 @@
 //
 // All HBM-bound: coalesced 16-byte vectors, a full warp per moved (K | V) row pair.
 #include "common.cuh"
+#include "tc_util.cuh"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 namespace cascade {
 
@@ -93,214 +98,314 @@ void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, i
   select_resolve_kernel<<<blocks, 256, 0, st>>>(g, p, begin, end, mu, s);
 }
 
-// maint_kernel: one block (8 warps) = one item for one (b, g).  Warp w owns moves 8w .. 8w+7 of
-// the item; lane j < 8 resolves move j (source, destination, mu, origin stay in its registers).
-// Every move of an item reads a resident slot; all rows go to shared memory before publishing.
-template <typename T>
-__global__ void __launch_bounds__(256, 6) maint_kernel(Geometry g, PlanDev p, MaintItems it, StateDev<T> sd,
-                                                       const float* __restrict__ s) {
-  constexpr int kPerWarp = kMaintMoves / 8;
-  extern __shared__ __align__(16) int4 s_rows[];          // [kMaintMoves][2 * nvec]
-  __shared__ uint32_t s_ticket, s_moved;
-  const int BG = g.B * g.Hkv;
-  const int bg = (int)(blockIdx.x % (unsigned)BG);
-  // per-(b, g) start-order ticket: a block only waits on items of its (b, g) that started before it
-  if (threadIdx.x == 0) { s_ticket = atomicAdd(it.ticket + bg, 1u); s_moved = 0; }
-  __syncthreads();
-  const int item = (int)(s_ticket - it.ticket_base);
-  const int4* rec = it.rec + (size_t)item * (1 + kMaintMoves);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e = warp * kPerWarp + lane;
-  // header and this lane's move record load together (records are padded to kMaintMoves)
-  const int4 hd = rec[0];                                  // n_moves, dep_lo, dep_hi, phase
-  const int4 mv = rec[1 + (lane < kPerWarp ? e : 0)];     // dst, ref, cand, inc
-  const long long sbase = (long long)bg * g.S_tot;
-  const double* mu = sd.mu + sbase;
-  const float* s_bg = s + (long long)bg * (g.S_tot + g.m);
-  const int nvec = g.d * (int)sizeof(T) / 16;             // vectors per K (or V) row
+constexpr int kChunkPerWarp = 2;
 
-  int32_t my_dst = -1, my_src = 0;
-  double my_mu = 0.0;
-  int64_t my_org = 0;
-  if (lane < kPerWarp && e < hd.x) {
-    int32_t src = mv.y;
-    if (src < 0) {
-      if (it.inline_sel) {
-        // winner of a depth-0 selection: cand if mu(cand) > mu(inc), strict (Q2); both
-        // operands' mu and origin are loaded together
-        const double mc = src_mu(g, mv.z, mu, s_bg), mi = src_mu(g, mv.w, mu, s_bg);
-        const int64_t oc = mv.z < g.S_tot ? sd.origin[sbase + mv.z] : g.t0 + (mv.z - g.S_tot);
-        const int64_t oi = mv.w < g.S_tot ? sd.origin[sbase + mv.w] : g.t0 + (mv.w - g.S_tot);
-        const bool cw = mc > mi;
-        src = cw ? mv.z : mv.w;
-        my_mu = cw ? mc : mi;
-        my_org = cw ? oc : oi;
-      } else {
-        src = p.resolved[(long long)bg * p.sel_cap + (-src - 1)];
-        my_mu = src_mu(g, src, mu, s_bg);
-        my_org = src < g.S_tot ? sd.origin[sbase + src] : g.t0 + (src - g.S_tot);
-      }
-    } else {
-      my_mu = src_mu(g, src, mu, s_bg);                    // folded (Q9) or a new token's s
-      my_org = src < g.S_tot ? sd.origin[sbase + src] : g.t0 + (src - g.S_tot);
-    }
-    if (src != mv.x) {                                     // resident won its selection: stays
-      my_dst = mv.x;
-      my_src = src;
-    }
+// maint_coop_kernel: the whole chunk's moves in ONE cooperative launch, no per-item ordering.
+// Moves that read a resident slot ("staged": evictees carried down a level, selections) are
+// split into rounds of at most gridDim.x * rows-per-block (x) b*g pairs, in per-(b, g) phase
+// order.  Round: every block loads its pairs' source rows into shared memory (cp.async) and
+// their mu / origin (selections resolved here, strict '>'), grid barrier, stores them.
+// Readers of a slot always come before its writer in phase order (they fill deeper
+// sub-caches), so a slot written in round k was read in a round <= k, before that round's
+// barrier.  Moves that read only chunk rows (never overwritten) fill the shared-memory rows the
+// last round leaves free -- loaded with it, stored after its barrier -- and any excess streams
+// through registers afterwards.
+constexpr int kCoopThreads = 512;
+// optional per-block timeline (globaltimer ns) for tuning: CASCADE_MAINT_TRACE=1
+__device__ unsigned long long* g_maint_trace = nullptr;
+__device__ __forceinline__ void trace_mark(int k) {
+  if (g_maint_trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_maint_trace[blockIdx.x * 8 + k] = t;
   }
-  const uint32_t any = __ballot_sync(0xffffffffu, my_dst >= 0);
-  const int gg = bg % g.Hkv, b = bg / g.Hkv;
-#pragma unroll
-  for (int j = 0; j < kPerWarp; ++j) {
-    const int32_t sj = __shfl_sync(0xffffffffu, my_src, j);
-    if (!((any >> j) & 1u)) continue;
-    const T *ks, *vs;
-    if (sj < g.S_tot) {
-      ks = sd.k_raw + (sbase + sj) * g.d;
-      vs = sd.v + (sbase + sj) * g.d;
-    } else {                                               // a selection won by a chunk row
-      const int r = sj - g.S_tot;
-      ks = sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-      vs = sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-    }
-    int4* row = s_rows + (warp * kPerWarp + j) * 2 * nvec;
-    for (int i = lane; i < 2 * nvec; i += 32) {
-      const int4* gsrc = i < nvec ? reinterpret_cast<const int4*>(ks) + i
-                                  : reinterpret_cast<const int4*>(vs) + (i - nvec);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc_smem_u32(row + i)), "l"(gsrc)
-                   : "memory");
-    }
+}
+template <typename T, int VPL>
+__global__ void __launch_bounds__(kCoopThreads, 2) maint_coop_kernel(Geometry g, PlanDev p, MaintItems it,
+                                                                     StateDev<T> sd, const float* __restrict__ s) {
+  extern __shared__ __align__(16) int4 s_rows[];          // [it.rows_per_block][2 * nvec]
+  const int R = it.rows_per_block;
+  double* s_mu = reinterpret_cast<double*>(s_rows + (size_t)R * 2 * (g.d * sizeof(T) / 16));
+  int64_t* s_org = reinterpret_cast<int64_t*>(s_mu + R);
+  long long* s_doff = reinterpret_cast<long long*>(s_org + R);   // destination flat row, -1: none
+  __shared__ uint32_t s_moved;
+  __shared__ __align__(8) uint64_t s_bar;                  // row loads of the current round
+  const int BG = g.B * g.Hkv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kCoopThreads / 32;
+  const uint32_t row_bytes = (uint32_t)(g.d * sizeof(T));  // one K (or V) row
+  const int nvec = g.d * (int)sizeof(T) / 16;             // vectors per K (or V) row
+  const uint32_t n = (uint32_t)it.n_staged, nc = (uint32_t)it.n_chunk;
+  const uint32_t total = n * (uint32_t)BG;                // staged (move, b*g) pairs, b*g-major
+  const uint32_t ctotal = nc * (uint32_t)BG;              // chunk-row pairs (both < 2^31)
+  const uint32_t G = gridDim.x;
+  const uint32_t per_round = G * (uint32_t)R;
+  const uint32_t rounds = total ? (total + per_round - 1) / per_round : (ctotal ? 1u : 0u);
+  if (threadIdx.x == 0) {
+    s_moved = 0;
+    tc::mbar_init(&s_bar, kCoopThreads);
+    tc::fence_mbar_init();
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-  // every loaded value must have ARRIVED before this block publishes, or a store of a later
-  // item could overtake a load still in flight.  The rows are in shared memory (waited above);
-  // the register operands are folded into one word that feeds the barrier's predicate
-  // (consuming a register waits for its load).
-  const uint32_t sink = (uint32_t)__double2loint(my_mu) ^ (uint32_t)my_org;
-  __syncthreads_or(sink == 0x9E3779B9u);
-  if (warp == 0) {
-    if (lane == 0) {
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(it.flags + (size_t)item * BG + bg), "r"(it.epoch)
-                   : "memory");
-    }
-    // wait for the items that read this item's destinations (host-computed, all earlier)
-    for (int j = hd.y + lane; j < hd.z; j += 32) {
-      const uint32_t* f = it.flags + (size_t)j * BG + bg;
+  __syncthreads();
+  trace_mark(0);
+  uint32_t bar = it.barrier_base;
+  // grid barrier.  After a load phase only READS precede it, all complete (rows waited on, the
+  // register operands stored to shared memory): a relaxed arrive suffices and no store can be
+  // issued before the spin observes every arrival.  Between rounds it also orders the
+  // previous round's stores (full fences).
+  auto grid_barrier = [&](bool fenced) {
+    __syncthreads();
+    trace_mark(3);
+    bar += G;
+    if (threadIdx.x == 0) {
+      if (fenced) __threadfence();
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(it.barrier) : "memory");
       uint32_t v;
       while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v == it.epoch) break;
-        __nanosleep(20);
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(it.barrier) : "memory");
+        if ((int32_t)(v - bar) >= 0) break;
+      }
+      if (fenced) __threadfence();
+    }
+    __syncthreads();
+  };
+  // chunk-row pairs beyond the last round's spare rows ("overflow"): kChunkPerWarp per warp
+  // through registers; the first batch is loaded before the last barrier and stored after it
+  const uint32_t gw = blockIdx.x * kWarps + warp, nw = G * kWarps;
+  int4 cbuf[kChunkPerWarp][VPL];
+  int32_t cdst[kChunkPerWarp], csrc[kChunkPerWarp], cbg[kChunkPerWarp];
+  auto chunk_load = [&](uint32_t w0) {
+#pragma unroll
+    for (int u = 0; u < kChunkPerWarp; ++u) {
+      const uint32_t pi = w0 + u;
+      cdst[u] = -1;
+      if (pi >= ctotal) continue;
+      const int bg = (int)(pi / nc);
+      const int4 mv = it.chunk[pi - (uint32_t)bg * nc];
+      const float* sbg = s + (long long)bg * (g.S_tot + g.m);
+      int32_t sr = mv.y;
+      if (sr < 0)
+        sr = it.inline_sel ? ((double)sbg[mv.z] > (double)sbg[mv.w] ? mv.z : mv.w)   // P:615, strict
+                           : p.resolved[(long long)bg * p.sel_cap + (-sr - 1)];
+      cdst[u] = mv.x; csrc[u] = sr; cbg[u] = bg;
+      const int r = sr - g.S_tot, gg = bg % g.Hkv, b = bg / g.Hkv;
+      const int4* ks = reinterpret_cast<const int4*>(sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
+      const int4* vs = reinterpret_cast<const int4*>(sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
+#pragma unroll
+      for (int h = 0; h < VPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < nvec) cbuf[u][h] = __ldcs(ks + i);
+        else if (i < 2 * nvec) cbuf[u][h] = __ldcs(vs + i - nvec);
       }
     }
+  };
+  auto chunk_store = [&]() {
+#pragma unroll
+    for (int u = 0; u < kChunkPerWarp; ++u) {
+      if (cdst[u] < 0) continue;
+      const long long sb = (long long)cbg[u] * g.S_tot;
+      int4* kd = reinterpret_cast<int4*>(sd.k_raw + (sb + cdst[u]) * g.d);
+      int4* vd = reinterpret_cast<int4*>(sd.v + (sb + cdst[u]) * g.d);
+#pragma unroll
+      for (int h = 0; h < VPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < nvec) __stcs(kd + i, cbuf[u][h]);
+        else if (i < 2 * nvec) __stcs(vd + i - nvec, cbuf[u][h]);
+      }
+      if (lane == 0) {
+        sd.mu[sb + cdst[u]] = (double)s[(long long)cbg[u] * (g.S_tot + g.m) + csrc[u]];   // mu = s
+        sd.origin[sb + cdst[u]] = g.t0 + (csrc[u] - g.S_tot);
+      }
+    }
+  };
+  // overflow pairs [ov0, ctotal): warp gw takes batches ov0 + (gw + k nw) kChunkPerWarp
+  uint32_t ov0 = ctotal;
+  // chunk-row pairs held in shared memory by the last round: cq per block
+  uint32_t cq = 0;
+  uint32_t moved = 0;
+  for (uint32_t rd = 0; rd < rounds; ++rd) {
+    const uint32_t r0 = rd * per_round;
+    const bool last = rd + 1 == rounds;
+    // this round's staged pairs, spread evenly over the blocks (<= R each)
+    const uint32_t in_round = total > r0 ? min(per_round, total - r0) : 0u;
+    const uint32_t q = (in_round + G - 1) / G;
+    const uint32_t lo = r0 + blockIdx.x * q;
+    const int cnt = (int)(blockIdx.x * q < in_round ? min(q, in_round - blockIdx.x * q) : 0u);
+    int ccnt = 0;
+    uint32_t clo = 0;
+    if (last) {
+      cq = min((uint32_t)R - q, (ctotal + G - 1) / G);
+      clo = blockIdx.x * cq;
+      ccnt = (int)(clo < ctotal ? min(cq, ctotal - clo) : 0u);
+      ov0 = min(ctotal, G * cq);
+      chunk_load(ov0 + gw * kChunkPerWarp);               // first overflow batch: loads in flight now
+    }
+    const int rows = cnt + ccnt;
+    // phase A: one thread per row (rows <= blockDim) resolves its source (selections: strict
+    // '>', Q2), loads mu / origin, and issues the row's two bulk copies (K, V) into
+    // shared memory; every thread arrives once on the round's mbarrier
+    {
+      const int j = threadIdx.x;
+      bool issued = false;
+      if (j < rows) {
+        const bool st = j < cnt;
+        const uint32_t pi = st ? lo + (uint32_t)j : clo + (uint32_t)(j - cnt);
+        const uint32_t nn = st ? n : nc;
+        const int bg = (int)(pi / nn);
+        const int4 mv = (st ? it.staged : it.chunk)[pi - (uint32_t)bg * nn];   // dst, ref, cand, inc
+        const long long sb = (long long)bg * g.S_tot;
+        const double* mu = sd.mu + sb;
+        const float* sbg = s + (long long)bg * (g.S_tot + g.m);
+        int32_t src = mv.y;
+        if (src < 0) {
+          if (it.inline_sel) {
+            const bool cw = src_mu(g, mv.z, mu, sbg) > src_mu(g, mv.w, mu, sbg);
+            src = cw ? mv.z : mv.w;
+          } else {
+            src = p.resolved[(long long)bg * p.sel_cap + (-src - 1)];
+          }
+        }
+        const bool mv_row = src != mv.x;                   // resident won its selection: stays
+        moved += (st && mv_row) ? 1u : 0u;                  // chunk-row moves: counted by the host
+        s_doff[j] = mv_row ? sb + mv.x : -1;
+        if (mv_row) {
+          const T *ks, *vs;
+          if (src < g.S_tot) {
+            ks = sd.k_raw + (sb + src) * g.d;
+            vs = sd.v + (sb + src) * g.d;
+          } else {
+            const int r = src - g.S_tot, gg = bg % g.Hkv, b = bg / g.Hkv;
+            ks = sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
+            vs = sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
+          }
+          uint8_t* row = reinterpret_cast<uint8_t*>(s_rows + (size_t)j * 2 * nvec);
+          tc::mbar_expect_tx(&s_bar, 2 * row_bytes);
+          tc::bulk_load(row, ks, row_bytes, &s_bar);
+          tc::bulk_load(row + row_bytes, vs, row_bytes, &s_bar);
+          issued = true;
+          s_mu[j] = src_mu(g, src, mu, sbg);               // folded (Q9) or a new token's s
+          s_org[j] = src < g.S_tot ? sd.origin[sb + src] : g.t0 + (src - g.S_tot);
+        }
+      }
+      if (!issued) tc::mbar_arrive(&s_bar);
+    }
+    trace_mark(1);
+    tc::mbar_wait(&s_bar, rd & 1u);
+    trace_mark(2);
+    if (total) grid_barrier(false);                        // every source of this round is read
+    else __syncthreads();
+    trace_mark(4);
+    // phase B: the row's thread bulk-stores K and V from shared memory, then mu and origin
+    tc::fence_proxy_async_smem();
+    {
+      const int j = threadIdx.x;
+      if (j < rows && s_doff[j] >= 0) {
+        const long long doff = s_doff[j];
+        const uint8_t* row = reinterpret_cast<const uint8_t*>(s_rows + (size_t)j * 2 * nvec);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sd.k_raw + doff * g.d),
+                     "r"(tc::smem_u32(row)), "r"(row_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sd.v + doff * g.d),
+                     "r"(tc::smem_u32(row + row_bytes)), "r"(row_bytes)
+                     : "memory");
+        sd.mu[doff] = s_mu[j];
+        sd.origin[doff] = s_org[j];
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (last) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem stays valid
+      else asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");            // writes done
+    }
+    if (last) chunk_store();
+    else grid_barrier(true);                               // rows reused; stores ordered
   }
+  // remaining overflow batches (the first one went with the last round)
+  for (uint32_t w0 = ov0 + (gw + nw) * kChunkPerWarp; w0 < ctotal; w0 += nw * kChunkPerWarp) {
+    chunk_load(w0);
+    chunk_store();
+  }
+  if (moved) atomicAdd(&s_moved, moved);
   __syncthreads();
-  if (lane == 0 && any) atomicAdd(&s_moved, (uint32_t)__popc(any));
-#pragma unroll
-  for (int j = 0; j < kPerWarp; ++j) {
-    const int32_t dj = __shfl_sync(0xffffffffu, my_dst, j);
-    if (!((any >> j) & 1u)) continue;
-    T* kd = sd.k_raw + (sbase + dj) * g.d;
-    T* vd = sd.v + (sbase + dj) * g.d;
-    const int4* row = s_rows + (warp * kPerWarp + j) * 2 * nvec;
-    for (int i = lane; i < 2 * nvec; i += 32) {
-      if (i < nvec) __stcs(reinterpret_cast<int4*>(kd) + i, row[i]);
-      else __stcs(reinterpret_cast<int4*>(vd) + i - nvec, row[i]);
-    }
-  }
-  if (my_dst >= 0) {
-    sd.mu[sbase + my_dst] = my_mu;
-    sd.origin[sbase + my_dst] = my_org;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_moved) atomicAdd(it.moved + bg, (unsigned long long)s_moved);
+  trace_mark(5);
+  if (threadIdx.x == 0 && s_moved) atomicAdd(it.moved + blockIdx.x % BG, (unsigned long long)s_moved);
 }
 
-// chunk_moves_kernel: moves that read no resident slot (chunk tokens entering C_1 or the sinks;
-// selections between two chunk rows).  Launched after maint_kernel, so every resident read of
-// the chunk is done; no ordering among them.  One warp per kChunkPerWarp (move, b*g) pairs, all
-// loads in flight before the stores.
-constexpr int kChunkPerWarp = 4;
 template <typename T>
-__global__ void __launch_bounds__(256) chunk_moves_kernel(Geometry g, PlanDev p, MaintItems it, StateDev<T> sd,
-                                                          const float* __restrict__ s) {
-  const int BG = g.B * g.Hkv;
-  const int lane = threadIdx.x & 31;
-  const int bg = blockIdx.y;
-  const int w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kChunkPerWarp;
-  const float* s_bg = s + (long long)bg * (g.S_tot + g.m);
-  const long long sbase = (long long)bg * g.S_tot;
-  const int gg = bg % g.Hkv, b = bg / g.Hkv;
-  const int nvec = g.d * (int)sizeof(T) / 16;
-  int4 buf[kChunkPerWarp][2];
-  int32_t dst[kChunkPerWarp], src[kChunkPerWarp];
-#pragma unroll
-  for (int u = 0; u < kChunkPerWarp; ++u) {
-    const int e = w0 + u;
-    dst[u] = -1;
-    if (e >= it.n_chunk) continue;
-    const int4 mv = it.chunk[e];                           // dst, ref, cand, inc
-    int32_t sr = mv.y;
-    if (sr < 0) {
-      sr = it.inline_sel ? ((double)s_bg[mv.z] > (double)s_bg[mv.w] ? mv.z : mv.w)   // P:615, strict
-                         : p.resolved[(long long)bg * p.sel_cap + (-sr - 1)];
-    }
-    dst[u] = mv.x; src[u] = sr;
-    const int r = sr - g.S_tot;
-    const int4* ks = reinterpret_cast<const int4*>(sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
-    const int4* vs = reinterpret_cast<const int4*>(sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = lane + 32 * h;
-      if (i < nvec) buf[u][h] = __ldcs(ks + i);
-      else if (i < 2 * nvec) buf[u][h] = __ldcs(vs + i - nvec);
+size_t maint_coop_smem(int d, int rows) {
+  return (size_t)rows * 2 * d * sizeof(T) + (size_t)rows * (8 + 8 + 8) + 16;
+}
+
+// Grid of the cooperative maintenance launch: co-resident blocks (2 per SM) and the rows each
+// stages per round.
+template <typename T>
+MaintGrid maint_coop_grid(int d) {
+  static MaintGrid mg[2] = {};
+  MaintGrid& m = mg[d == 128 ? 1 : 0];
+  if (m.blocks) return m;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int rows = std::min(kCoopThreads, (int)((110 * 1024 - 16) / (2 * d * sizeof(T) + 24)));
+  const size_t smem = maint_coop_smem<T>(d, rows);
+  auto kern = maint_coop_kernel<T, 1>;
+  if (2 * d * sizeof(T) / 16 > 32) kern = maint_coop_kernel<T, 2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCoopThreads, smem);
+  m.blocks = std::max(1, std::min(per_sm, 2)) * sms;
+  m.rows_per_block = rows;
+  return m;
+}
+
+template <typename T>
+void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
+                  cudaStream_t st) {
+  if (it.n_staged <= 0 && it.n_chunk <= 0) return;
+  const MaintGrid mg = maint_coop_grid<T>(g.d);
+  it.rows_per_block = mg.rows_per_block;
+  const size_t smem = maint_coop_smem<T>(g.d, mg.rows_per_block);
+  void* args[] = {(void*)&g, (void*)&p, (void*)&it, (void*)&sd, (void*)&s};
+  const void* kern = 2 * g.d * sizeof(T) / 16 > 32 ? (const void*)maint_coop_kernel<T, 2>
+                                                   : (const void*)maint_coop_kernel<T, 1>;
+  static unsigned long long* trace = nullptr;
+  static int trace_on = -1, trace_n = 0;
+  if (trace_on < 0) {
+    const char* e = std::getenv("CASCADE_MAINT_TRACE");
+    trace_on = e && std::atoi(e) > 0 ? std::atoi(e) : 0;
+    if (trace_on) {
+      cudaMalloc(&trace, (size_t)mg.blocks * 8 * 8);
+      cudaMemcpyToSymbol(g_maint_trace, &trace, sizeof(trace));
     }
   }
-#pragma unroll
-  for (int u = 0; u < kChunkPerWarp; ++u) {
-    if (dst[u] < 0) continue;
-    int4* kd = reinterpret_cast<int4*>(sd.k_raw + (sbase + dst[u]) * g.d);
-    int4* vd = reinterpret_cast<int4*>(sd.v + (sbase + dst[u]) * g.d);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = lane + 32 * h;
-      if (i < nvec) __stcs(kd + i, buf[u][h]);
-      else if (i < 2 * nvec) __stcs(vd + i - nvec, buf[u][h]);
-    }
-    if (lane == 0) {
-      sd.mu[sbase + dst[u]] = (double)s_bg[src[u]];        // new token: mu = s
-      sd.origin[sbase + dst[u]] = g.t0 + (src[u] - g.S_tot);
-    }
+  cudaLaunchCooperativeKernel(kern, dim3(mg.blocks), dim3(kCoopThreads), args, smem, st);
+  if (trace_on && ++trace_n == trace_on) {     // dump the n-th launch: per-block marks, ns
+    std::vector<unsigned long long> h((size_t)mg.blocks * 8);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < mg.blocks; ++b) t0 = std::min(t0, h[b * 8]);
+    std::fprintf(stderr, "maint trace (staged %d chunk %d): block start A1 A2wait barrier_in barrier_out end\n",
+                 it.n_staged, it.n_chunk);
+    for (int b = 0; b < mg.blocks; b += 1)
+      std::fprintf(stderr, "%d %llu %llu %llu %llu %llu %llu\n", b, h[b * 8] - t0, h[b * 8 + 1] - t0,
+                   h[b * 8 + 2] - t0, h[b * 8 + 3] - t0, h[b * 8 + 4] - t0, h[b * 8 + 5] - t0);
   }
 }
 
 template <typename T>
-void launch_maint(const Geometry& g, const PlanDev& p, const MaintItems& it, int n_items, StateDev<T> sd,
-                  const float* s, cudaStream_t st) {
-  const int BG = g.B * g.Hkv;
-  if (n_items > 0) {
-    const size_t smem = (size_t)kMaintMoves * 2 * g.d * sizeof(T);
-    static bool attr_set[2] = {false, false};
-    bool& done = attr_set[sizeof(T) == 2];
-    if (!done) {   // full shared-memory carveout: 6 blocks of 32 KB per SM
-      cudaFuncSetAttribute(maint_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cudaFuncSetAttribute(maint_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      done = true;
-    }
-    maint_kernel<T><<<n_items * BG, 256, smem, st>>>(g, p, it, sd, s);
-  }
-  if (it.n_chunk > 0) {
-    const int warps = (it.n_chunk + kChunkPerWarp - 1) / kChunkPerWarp;
-    chunk_moves_kernel<T><<<dim3((warps + 7) / 8, BG), 256, 0, st>>>(g, p, it, sd, s);
-  }
+int maint_barriers(const Geometry& g, const MaintItems& it) {
+  const MaintGrid mg = maint_coop_grid<T>(g.d);
+  const long long total = (long long)it.n_staged * g.B * g.Hkv;
+  const long long per_round = (long long)mg.blocks * mg.rows_per_block;
+  const long long rounds = (total + per_round - 1) / per_round;
+  return (int)(rounds > 0 ? 2 * rounds - 1 : 0) * mg.blocks;
 }
 
-template void launch_maint<float>(const Geometry&, const PlanDev&, const MaintItems&, int, StateDev<float>,
-                                  const float*, cudaStream_t);
-template void launch_maint<__nv_bfloat16>(const Geometry&, const PlanDev&, const MaintItems&, int,
-                                          StateDev<__nv_bfloat16>, const float*, cudaStream_t);
+template void launch_maint<float>(const Geometry&, const PlanDev&, MaintItems, StateDev<float>, const float*,
+                                  cudaStream_t);
+template int maint_barriers<float>(const Geometry&, const MaintItems&);
+template int maint_barriers<__nv_bfloat16>(const Geometry&, const MaintItems&);
+template void launch_maint<__nv_bfloat16>(const Geometry&, const PlanDev&, MaintItems, StateDev<__nv_bfloat16>,
+                                          const float*, cudaStream_t);
 
 __global__ void positions_kernel(Geometry g, int32_t* __restrict__ pe) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.S_tot; x += gridDim.x * blockDim.x)
