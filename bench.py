@@ -376,8 +376,11 @@ def main():
         "attention_total": {"kernels": "attn_fwd + attn_score", "achieved": w1 / ((t1 + t2) / 1e3) / 1e12 if t1 + t2 > 0 else 0,
                             "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                             "frac": (w1 / ((t1 + t2) / 1e3) / 1e12 / peaks["bf16_sus"]) if t1 + t2 > 0 else 0},
-        "maintenance": {"bound": "hbm", "achieved": rm / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
-                        "frac": rm / 1e9 / peaks["hbm"]},
+        "maintenance": {"kernel": "maint_coop_kernel (Alg. 2 admission, selections, K/V/mu/origin moves; "
+                                  "the EMA fold runs in attn_score's epilogue)",
+                        "bound": "hbm", "achieved": rm / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
+                        "frac": rm / 1e9 / peaks["hbm"],
+                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)"},
     }
     share = {k: v["ms_per_step"] / ms_step for k, v in kern.items()}
 
