@@ -380,11 +380,12 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int kb = 0; kb < KB; ++kb)
           tc::tma_load_2d(sK + (w * KB + kb) * kTileBytes, &tm_k, k_full, kb * 64, krow);
       }
-      for (int i = 0; i < n_items; ++i) {
+      for (int i = 0, qi = 0, hi = 0; i < n_items; ++i) {
         const int st = i % kStages, u = i / kStages;
         if (i >= kStages) tc::mbar_wait(q_empty + st, (u - 1) & 1);
-        const int hh = gkv * p.G + i / per_head;
-        const int q0 = (qt_begin + i % per_head) * 128;
+        const int hh = gkv * p.G + hi;
+        const int q0 = (qt_begin + qi) * 128;
+        if (++qi == per_head) { qi = 0; ++hi; }
         const int qrow = (int)(((long long)b * p.Hq + hh) * p.M + q0);
         tc::mbar_expect_tx(q_full + st, KB * kTileBytes + 512);
         for (int kb = 0; kb < KB; ++kb)
@@ -442,9 +443,10 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
     for (int hh = 0; hh < p.G; ++hh) my_acc[hh * 128 + r] = 0.f;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    int qi = 0, hcur = 0;                                 // item i = (head hcur, q-tile qi), no division
     for (int i = 0; i < n_items; ++i) {
       const int sb2 = i & 1, st = i % kStages;
-      const int q0 = (qt_begin + i % per_head) * 128 + half * 64;   // first query of this half
+      const int q0 = (qt_begin + qi) * 128 + half * 64;   // first query of this half
       const float* bq = sb + st * 128 + half * 64;
       tc::mbar_wait(q_full + st, (i / kStages) & 1);      // biases of this item have landed
       tc::mbar_wait(s_full + sb2, (i >> 1) & 1);
@@ -464,10 +466,12 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) { tc::mbar_arrive(s_free + sb2); tc::mbar_arrive(q_empty + st); }
-      if ((i + 1) % per_head == 0) {                       // this half's sum for the head
+      if (++qi == per_head) {                              // this half's sum for the head
         const float2 s01 = __fadd2_rn(a0, a1), s23 = __fadd2_rn(a2, a3);
-        my_acc[(i / per_head) * 128 + r] = (s01.x + s01.y) + (s23.x + s23.y);
+        my_acc[hcur * 128 + r] = (s01.x + s01.y) + (s23.x + s23.y);
         a0 = a1 = a2 = a3 = make_float2(0.f, 0.f);
+        qi = 0;
+        ++hcur;
       }
     }
     tc::named_bar_sync(1, 544);                           // all halves' per-head sums in smem
@@ -517,16 +521,19 @@ void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtens
                           cudaStream_t st) {
   dim3 grid((p.n_res_tiles + 1) / 2 + ((p.m + 127) / 128 + 1) / 2, p.B * p.Hkv);
   const size_t smem = attn_score_tc_smem(d, p.G);
-  // exp2 pairs on the FMA pipe per 16 (degree-4 polynomial): measured 2.50 / 2.30 / 2.25 / 2.16 /
-  // 2.20 / 2.21 / 2.44 ms per steady-state chunk for 0 / 2 / 3 / 4 / 5 / 6 / 8 (scripts/kbench.py)
+  // exp2 pairs on the FMA pipe per 16: measured (degree-4 polynomial) 2.50 / 2.30 / 2.25 / 2.16 /
+  // 2.20 / 2.21 / 2.44 ms per steady-state chunk for 0 / 2 / 3 / 4 / 5 / 6 / 8; after removing the
+  // runtime divisions from the item loop, degree 4 at 4/16: 2.03 ms, degree 3 (7.5e-5 rel.) at
+  // 3 / 4 / 5 of 16: 2.09 / 2.01 / 2.05 ms (scripts/kbench.py).  Prefetching both 32-column TMEM
+  // chunks before the math (64 more live registers) measured 2.16 ms.
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 640, smem, st>>>(tq, tk, p);
   };
   if (d == 128) {
-    go(attn_score_tc_kernel<128, 4, 4>);
+    go(attn_score_tc_kernel<128, 4, 3>);
   } else {
-    go(attn_score_tc_kernel<64, 4, 4>);
+    go(attn_score_tc_kernel<64, 4, 3>);
   }
 }
 
