@@ -63,8 +63,7 @@ SMALL = [  # (alpha, N, c, B, Hkv, dtype, strides)
 
 
 @pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", SMALL)
-def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides):
-    d = 64
+def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=64):
     cfg = C.CascadeConfig(batch=B, num_q_heads=Hkv, num_kv_heads=Hkv, head_dim=d, sink_size=alpha,
                           cache_size=N * c, num_cascades=N, max_stride=max(strides), dtype=dtype,
                           ema_gamma=0.99)
@@ -82,6 +81,21 @@ def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides):
         orc.update_with_scores(0, _np(k), _np(v), s.astype(np.float64))
         torch.cuda.synchronize()
         _compare_state(gpu.state(0), orc.state(0))
+
+
+# Geometries whose chunks move more resident-reading rows than one cooperative maintenance
+# round stages GPU-wide (2 CTAs x ~107 fp32 d=128 rows per SM): several rounds, each with its
+# own grid barrier, in phase order; one with m <= c (depth-0 selections resolved inline) and one
+# with m > c (nested selections resolved beforehand).
+MULTI_ROUND = [
+    (8, 3, 8192, 2, 4, "f32", [8192] * 4),
+    (8, 3, 4096, 2, 4, "f32", [4096, 8192, 8192]),
+]
+
+
+@pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", MULTI_ROUND)
+def test_score_injection_multi_round_maintenance(alpha, N, c, B, Hkv, dtype, strides):
+    test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=128)
 
 
 def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_advance=0):
