@@ -110,8 +110,8 @@ Sizes compute_sizes(const cascade_config& c) {
   z.dec_logits = z.dec_part_o = z.dec_part_ml = 0;
   if (c.dtype == CASCADE_BF16) {
     const size_t bgs = B * Hk;
-    size_t ns = (148 * 7 + bgs - 1) / bgs;
-    ns = std::max<size_t>(1, std::min<size_t>(ns, ((S / 128 + 2 * N + 2) + 1 + 3) / 4));
+    // the most splits decode_attn_nsplit may pick (k_decode.cu): <= 64, >= 4 tiles per split
+    const size_t ns = std::max<size_t>(1, std::min<size_t>(64, ((S / 128 + 2 * N + 2) + 1 + 3) / 4));
     z.dec_nsplit = (int32_t)ns;
     z.dec_logits = align_up(bgs * (S + 1) * G * 4);
     z.dec_part_o = align_up(bgs * ns * G * d * 4);

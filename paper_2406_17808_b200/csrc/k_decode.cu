@@ -17,6 +17,8 @@
 //                   insertion: the (at most one) selection and the (at most N+1) row moves,
 //                   deepest sub-cache first.
 #include "common.cuh"
+
+#include <cmath>
 #include "tc_util.cuh"
 
 namespace cascade {
@@ -487,10 +489,20 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
 }
 
 size_t decode_attn_nsplit(const DecodeParams& p) {
+  // splits per (b, g): minimise (waves of 1-CTA-per-SM CTAs) x (tiles per CTA + ~4 tiles of
+  // per-CTA pipeline fill / combine overhead); >= 4 tiles per split.  Measured at B = 64,
+  // Hkv = 8, 129 tiles (scripts/dbench.py): 1 / 2 / 3 / 4 / 5 / 6 / 8 / 12 splits ->
+  // 1.010 / 0.922 / 0.968 / 0.954 / 0.985 / 0.984 / 1.014 / 1.066 ms per step; the model picks 2.
   const int bgs = p.B * p.Hkv;
-  int ns = (148 * 7 + bgs - 1) / bgs;                     // ~7 waves at 1 CTA / SM
-  ns = std::max(1, std::min(ns, (p.n_tiles + 1 + 3) / 4)); // >= 4 tiles per split
-  return (size_t)ns;
+  const int cap = std::max(1, std::min(64, (p.n_tiles + 1 + 3) / 4));
+  int best = 1;
+  double best_cost = 1e300;
+  for (int ns = 1; ns <= cap; ++ns) {
+    const double waves = std::ceil((double)bgs * ns / 148.0);
+    const double cost = waves * ((double)(p.n_tiles + 1) / ns + 4.0);
+    if (cost < best_cost) { best_cost = cost; best = ns; }
+  }
+  return (size_t)best;
 }
 
 template <int G>
