@@ -163,6 +163,7 @@ struct cascade_handle {
   std::vector<int32_t> maint_reads;
   std::vector<int4> maint_staged, maint_chunk;
   bool fwd_pairs;           // pass 1 on CTA pairs (k_attn_tc2.cu); CASCADE_FWD_PAIRS=1 at init
+  bool fwd_pp;              // pass 1 with two query tiles per CTA (k_attn_pp.cu); CASCADE_FWD_PP
 };
 
 namespace {
@@ -289,6 +290,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->profiling = false;
   h->moved_seen = 0;
   { const char* e = std::getenv("CASCADE_FWD_PAIRS"); h->fwd_pairs = e && std::atoi(e) != 0; }
+  { const char* e = std::getenv("CASCADE_FWD_PP"); h->fwd_pp = e && std::atoi(e) != 0; }
   h->moved_chunk = 0;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
 
@@ -632,6 +634,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     {
       ProfScope ps(h, 1, st);
       if (g.d == 128 && h->fwd_pairs) launch_attn_fwd_tc2(tp, L.tm_q, L.tm_k64, L.tm_vs, L.tm_vc, st);
+      else if (g.d == 128 && h->fwd_pp) launch_attn_fwd_pp(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, st);
       else launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
       ps.finish(useful);
     }

@@ -334,19 +334,22 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   double* smu = reinterpret_cast<double*>(bars + 14);   // [2][128] EMA operands of the two key tiles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bgi = blockIdx.y;
+  // grid (b*g, pair): blocks launch x-fastest, so every (b, g)'s resident pairs go before the
+  // cheaper causal chunk pairs and the last, partial wave is made of the cheap ones
+  const int bgi = blockIdx.x;
+  const int pair = blockIdx.y;
   const int b = bgi / p.Hkv, gkv = bgi - b * p.Hkv;
   const long long bg = bgi;
   // pair -> tiles: resident pairs first, then chunk pairs
   const int n_res_pairs = (p.n_res_tiles + 1) / 2;
   const int n_chunk_tiles = (p.m + 127) / 128;
-  const bool resident = (int)blockIdx.x < n_res_pairs;
+  const bool resident = pair < n_res_pairs;
   int n_here, first;                                    // number of tiles in this pair, first tile
   if (resident) {
-    first = 2 * blockIdx.x;
+    first = 2 * pair;
     n_here = min(2, p.n_res_tiles - first);
   } else {
-    first = 2 * (blockIdx.x - n_res_pairs);             // chunk tile index
+    first = 2 * (pair - n_res_pairs);                   // chunk tile index
     n_here = min(2, n_chunk_tiles - first);
   }
   const int nqt = n_chunk_tiles;
@@ -519,7 +522,7 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
 
 void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, int d,
                           cudaStream_t st) {
-  dim3 grid((p.n_res_tiles + 1) / 2 + ((p.m + 127) / 128 + 1) / 2, p.B * p.Hkv);
+  dim3 grid(p.B * p.Hkv, (p.n_res_tiles + 1) / 2 + ((p.m + 127) / 128 + 1) / 2);
   const size_t smem = attn_score_tc_smem(d, p.G);
   // exp2 pairs on the FMA pipe per 16: measured (degree-4 polynomial) 2.50 / 2.30 / 2.25 / 2.16 /
   // 2.20 / 2.21 / 2.44 ms per steady-state chunk for 0 / 2 / 3 / 4 / 5 / 6 / 8; after removing the
