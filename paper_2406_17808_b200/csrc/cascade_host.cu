@@ -40,7 +40,6 @@ struct LayerBufs {
   uint32_t maint_barrier;   // host copy of the barrier counter (wrapping)
   CUtensorMap tm_q, tm_k, tm_vs, tm_vc;   // TMA maps of q_rot, k_rot, v (state), v_chunk
   CUtensorMap tm_kraw;                    // TMA map of the pre-RoPE key state (decode)
-  CUtensorMap tm_k64;                     // k_rot with 64-row boxes (pass 1 on CTA pairs)
 };
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -61,12 +60,12 @@ EncodeTiledFn encode_fn() {
 
 // 2D bf16 row-major [rows][d] map with 64 x 128 boxes and 128-byte swizzle (the UMMA K-major /
 // MN-major SW128 canonical layouts).
-bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d, uint32_t box_rows = 128) {
+bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {d, rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {64, 128};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -162,8 +161,6 @@ struct cascade_handle {
   // maintenance planning scratch
   std::vector<int32_t> maint_reads;
   std::vector<int4> maint_staged, maint_chunk;
-  bool fwd_pairs;           // pass 1 on CTA pairs (k_attn_tc2.cu); CASCADE_FWD_PAIRS=1 at init
-  bool fwd_pp;              // pass 1 with two query tiles per CTA (k_attn_pp.cu); CASCADE_FWD_PP
 };
 
 namespace {
@@ -289,8 +286,6 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->ring_pos = 0;
   h->profiling = false;
   h->moved_seen = 0;
-  { const char* e = std::getenv("CASCADE_FWD_PAIRS"); h->fwd_pairs = e && std::atoi(e) != 0; }
-  { const char* e = std::getenv("CASCADE_FWD_PP"); h->fwd_pp = e && std::atoi(e) != 0; }
   h->moved_chunk = 0;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }
 
@@ -347,8 +342,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
            make_map(&L.tm_k, L.k_rot, B * Hk * ((uint64_t)h->S_tot + M), d) &&
            make_map(&L.tm_vs, L.v, B * Hk * (uint64_t)h->S_tot, d) &&
            make_map(&L.tm_vc, L.v_chunk, B * Hk * M, d) &&
-           make_map(&L.tm_kraw, L.k_raw, B * Hk * (uint64_t)h->S_tot, d) &&
-           make_map(&L.tm_k64, L.k_rot, B * Hk * ((uint64_t)h->S_tot + M), d, 64);
+           make_map(&L.tm_kraw, L.k_raw, B * Hk * (uint64_t)h->S_tot, d);
     }
   }
   // RoPE table: (cos, sin)(pos * theta^(-2i/d)) computed in double, rounded to fp32 (Q11).
@@ -633,9 +627,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);
-      if (g.d == 128 && h->fwd_pairs) launch_attn_fwd_tc2(tp, L.tm_q, L.tm_k64, L.tm_vs, L.tm_vc, st);
-      else if (g.d == 128 && h->fwd_pp) launch_attn_fwd_pp(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, st);
-      else launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
+      launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
       ps.finish(useful);
     }
     {

@@ -163,11 +163,7 @@ void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, cons
                    cudaStream_t st);
 
 size_t attn_fwd_tc_smem(int d);
-// pass 1 with two query tiles per CTA (k_attn_pp.cu, d = 128)
-void launch_attn_fwd_pp(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvs,
-                        const CUtensorMap& tvc, cudaStream_t st);
-void launch_attn_fwd_tc2(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tvs,
-                         const CUtensorMap& tvc, cudaStream_t st);
+
 size_t attn_score_tc_smem(int d, int G);
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                         const CUtensorMap& tvs, const CUtensorMap& tvc, int d, cudaStream_t st);

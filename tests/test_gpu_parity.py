@@ -145,20 +145,6 @@ def test_cfg2_first_chunks_end_to_end_bf16():
     print(f"cfg2[0:6]: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e}")
 
 
-def test_cfg2_first_chunks_cta_pairs(monkeypatch):
-    """The opt-in CTA-pair pass 1 (tcgen05.mma.cta_group::2, k_attn_tc2.cu) on the same chunks."""
-    monkeypatch.setenv("CASCADE_FWD_PAIRS", "1")
-    worst_o, worst_s, _ = _run_end_to_end("cfg2_llama8b_4k", n_chunks=6, check_every=2)
-    assert worst_o <= O_TOL["bf16"] and worst_s <= S_RTOL
-
-
-def test_cfg2_first_chunks_ping_pong(monkeypatch):
-    """The opt-in two-query-tiles-per-CTA pass 1 (k_attn_pp.cu) on the same chunks."""
-    monkeypatch.setenv("CASCADE_FWD_PP", "1")
-    worst_o, worst_s, _ = _run_end_to_end("cfg2_llama8b_4k", n_chunks=6, check_every=2)
-    assert worst_o <= O_TOL["bf16"] and worst_s <= S_RTOL
-
-
 def test_cfg2_passkey_chunks_bf16():
     """A salient 5-token block mid-chunk makes the running row max jump (O rescaled in TMEM)."""
     # seed advanced once: the first seed's oracle audit saw a 3.9e-4 selection margin
