@@ -158,6 +158,22 @@ cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, con
                                            const void* k, const void* v, int32_t m, void* out,
                                            void* stream);
 
+/* Pipelined form of cascade_prefill_stride_host: enqueues the chunk and returns
+ * without synchronising.  Host->device copies run on a library copy stream into
+ * one of two staging sets (alternating per call), the step on `stream` after
+ * its inputs landed, the device->host copy of `out` on a second copy stream
+ * once the step is done -- so chunk c+1's inputs and chunk c-1's output move
+ * over PCIe while chunk c computes.  The caller keeps q/k/v/out valid and
+ * does not read `out` until cascade_host_wait returns.  One handle, one
+ * stream; chunks of all layers are processed in call order. */
+cascade_status cascade_prefill_stride_host_async(cascade_handle* h, int32_t layer, const void* q,
+                                                 const void* k, const void* v, int32_t m, void* out,
+                                                 void* stream);
+
+/* Blocks until every copy enqueued by cascade_prefill_stride_host_async has
+ * completed (all outputs are in host memory). */
+cascade_status cascade_host_wait(cascade_handle* h);
+
 /* Single-token step (Eq. 2) + update, m = 1.
  *   q [B, Hq, d], k/v [B, Hkv, d], out [B, Hq, d], device, dtype. */
 cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,

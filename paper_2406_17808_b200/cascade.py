@@ -75,6 +75,8 @@ def lib():
             "cascade_destroy": (None, [vp]),
             "cascade_prefill_stride": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
             "cascade_prefill_stride_host": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
+            "cascade_prefill_stride_host_async": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
+            "cascade_host_wait": (i32, [vp]),
             "cascade_decode": (i32, [vp, i32, vp, vp, vp, vp, vp]),
             "cascade_state": (i32, [vp, i32, ctypes.POINTER(_StateView), vp]),
             "cascade_update_with_scores": (i32, [vp, i32, vp, vp, i32, vp, vp]),
@@ -95,7 +97,8 @@ def lib():
 
 EXPORTED = ["cascade_status_string", "cascade_validate_config", "cascade_workspace_bytes",
             "cascade_init", "cascade_destroy", "cascade_prefill_stride",
-            "cascade_prefill_stride_host", "cascade_decode", "cascade_state",
+            "cascade_prefill_stride_host", "cascade_prefill_stride_host_async", "cascade_host_wait",
+            "cascade_decode", "cascade_state",
             "cascade_update_with_scores", "cascade_last_scores", "cascade_mirror_advance",
             "cascade_launch_count", "cascade_reset", "cascade_profile_enable",
             "cascade_profile_read"]
@@ -232,6 +235,20 @@ class Cascade:
                                                _ptr(out), _stream(stream))
         _check(rc, "cascade_prefill_stride_host")
         return out
+
+    def prefill_stride_host_async(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                  out: torch.Tensor, stream=None) -> torch.Tensor:
+        """Pipelined host-buffer step: returns at once; `out` is valid after host_wait()."""
+        m = q.shape[1]
+        for t in (q, k, v, out):
+            assert not t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        rc = lib().cascade_prefill_stride_host_async(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m,
+                                                     _ptr(out), _stream(stream))
+        _check(rc, "cascade_prefill_stride_host_async")
+        return out
+
+    def host_wait(self) -> None:
+        _check(lib().cascade_host_wait(self._h), "cascade_host_wait")
 
     def decode(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

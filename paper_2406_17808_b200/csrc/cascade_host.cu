@@ -126,8 +126,9 @@ Sizes compute_sizes(const cascade_config& c) {
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
-  z.total = z.per_layer * c.num_layers + z.rope_tab + z.tab_hi + z.tab_lo + z.stage_q + 2 * z.stage_kv +
-            z.stage_out;
+  // two staging sets: the synchronous host call uses set 0, the pipelined one alternates
+  z.total = z.per_layer * c.num_layers + z.rope_tab + z.tab_hi + z.tab_lo +
+            2 * (z.stage_q + 2 * z.stage_kv + z.stage_out);
   return z;
 }
 
@@ -144,7 +145,13 @@ struct cascade_handle {
   float2* rope_tab;
   float2* tab_hi;
   float2* tab_lo;
-  void *stage_q, *stage_k, *stage_v, *stage_out;
+  void *stage_q, *stage_k, *stage_v, *stage_out;           // set 0 (aliases stage[0])
+  struct Stage { void *q, *k, *v, *out; } stage[2];
+  // pipelined host path (cascade_prefill_stride_host_async): copy streams and per-set events
+  cudaStream_t h2d, d2h;
+  cudaEvent_t ev_in[2], ev_comp[2], ev_out[2];
+  bool stage_used[2];
+  int host_slot;
   Planner planner;
   Plan plan;
   int32_t* pinned[kRing];
@@ -259,6 +266,13 @@ void cascade_destroy(cascade_handle* h) {
     if (h->ring_ev[i]) cudaEventDestroy(h->ring_ev[i]);
     if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
   }
+  if (h->h2d) { cudaStreamSynchronize(h->h2d); cudaStreamDestroy(h->h2d); }
+  if (h->d2h) { cudaStreamSynchronize(h->d2h); cudaStreamDestroy(h->d2h); }
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+    if (h->ev_comp[i]) cudaEventDestroy(h->ev_comp[i]);
+    if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
+  }
   delete h;
 }
 
@@ -311,12 +325,25 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
   h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
-  h->stage_q = take(sz.stage_q); h->stage_k = take(sz.stage_kv);
-  h->stage_v = take(sz.stage_kv); h->stage_out = take(sz.stage_out);
+  for (int i = 0; i < 2; ++i) {
+    h->stage[i].q = take(sz.stage_q); h->stage[i].k = take(sz.stage_kv);
+    h->stage[i].v = take(sz.stage_kv); h->stage[i].out = take(sz.stage_out);
+  }
+  h->stage_q = h->stage[0].q; h->stage_k = h->stage[0].k;
+  h->stage_v = h->stage[0].v; h->stage_out = h->stage[0].out;
   h->mirrors.assign(cfg->num_layers, cascade_mirror{});
   h->m_last.assign(cfg->num_layers, 0);
 
   bool ok = true;
+  ok = ok && cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 2 && ok; ++i) {
+    ok = cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_comp[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+    h->stage_used[i] = false;
+  }
+  h->host_slot = 0;
   for (int i = 0; i < kRing && ok; ++i) {
     ok = cudaHostAlloc(reinterpret_cast<void**>(&h->pinned[i]), (size_t)sz.plan_ints * 4,
                        cudaHostAllocDefault) == cudaSuccess &&
@@ -700,6 +727,45 @@ cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, con
   if (cudaMemcpyAsync(out, h->stage_out, nq, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return CASCADE_ERR_CUDA;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_prefill_stride_host_async(cascade_handle* h, int32_t layer, const void* q,
+                                                 const void* k, const void* v, int32_t m, void* out,
+                                                 void* stream) {
+  cascade_status rc = check_call(h, layer, m);
+  if (rc != CASCADE_OK) return rc;
+  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = elem_size(h->cfg.dtype);
+  const size_t nq = (size_t)h->cfg.batch * m * h->cfg.num_q_heads * h->cfg.head_dim * es;
+  const size_t nk = (size_t)h->cfg.batch * m * h->cfg.num_kv_heads * h->cfg.head_dim * es;
+  const int slot = h->host_slot;
+  auto& S = h->stage[slot];
+  // the set is free once the device->host copy of its previous chunk is done
+  if (h->stage_used[slot] && cudaStreamWaitEvent(h->h2d, h->ev_out[slot], 0) != cudaSuccess) return CASCADE_ERR_CUDA;
+  if (cudaMemcpyAsync(S.q, q, nq, cudaMemcpyHostToDevice, h->h2d) != cudaSuccess ||
+      cudaMemcpyAsync(S.k, k, nk, cudaMemcpyHostToDevice, h->h2d) != cudaSuccess ||
+      cudaMemcpyAsync(S.v, v, nk, cudaMemcpyHostToDevice, h->h2d) != cudaSuccess ||
+      cudaEventRecord(h->ev_in[slot], h->h2d) != cudaSuccess ||
+      cudaStreamWaitEvent(st, h->ev_in[slot], 0) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  rc = cascade_prefill_stride(h, layer, S.q, S.k, S.v, m, S.out, stream);
+  if (rc != CASCADE_OK) return rc;
+  if (cudaEventRecord(h->ev_comp[slot], st) != cudaSuccess ||
+      cudaStreamWaitEvent(h->d2h, h->ev_comp[slot], 0) != cudaSuccess ||
+      cudaMemcpyAsync(out, S.out, nq, cudaMemcpyDeviceToHost, h->d2h) != cudaSuccess ||
+      cudaEventRecord(h->ev_out[slot], h->d2h) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  h->stage_used[slot] = true;
+  h->host_slot ^= 1;
+  return CASCADE_OK;
+}
+
+cascade_status cascade_host_wait(cascade_handle* h) {
+  if (!h) return CASCADE_ERR_INVALID_ARG;
+  if (cudaStreamSynchronize(h->h2d) != cudaSuccess || cudaStreamSynchronize(h->d2h) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
   return CASCADE_OK;
 }
 

@@ -249,3 +249,31 @@ def test_ragged_chunks_tensor_core_path(d):
         _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
     margins = orc.select_margins()
     assert margins.size == 0 or margins.min() > 1e-3
+
+
+def test_host_buffer_paths_match_device_path():
+    """cascade_prefill_stride_host and the pipelined cascade_prefill_stride_host_async (copies on
+    library streams, two staging sets) give the device path's outputs and state bit for bit."""
+    cfg = C.CascadeConfig(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=128, sink_size=4,
+                          cache_size=256, num_cascades=4, max_stride=64, dtype="bf16")
+    syn = Synth(2, 8, 2, 128, seed=21)
+    dev, syn_h, pipe = C.Cascade(cfg), C.Cascade(cfg), C.Cascade(cfg)
+    chunks = [syn.chunk(start, 64) for start in range(0, 7 * 64, 64)]
+    outs_dev = [_np(dev.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())) for q, k, v in chunks]
+    pinned = [tuple(t.pin_memory() for t in c) for c in chunks]
+    outs_sync = []
+    for q, k, v in pinned:
+        o = torch.empty_like(q).pin_memory()
+        syn_h.prefill_stride_host(0, q, k, v, o)
+        outs_sync.append(_np(o))
+    outs_pipe = [torch.empty_like(q).pin_memory() for q, _, _ in pinned]
+    for (q, k, v), o in zip(pinned, outs_pipe):
+        pipe.prefill_stride_host_async(0, q, k, v, o)
+    pipe.host_wait()
+    for a, b_, c in zip(outs_dev, outs_sync, outs_pipe):
+        np.testing.assert_array_equal(a, b_)
+        np.testing.assert_array_equal(a, _np(c))
+    torch.cuda.synchronize()
+    s_dev, s_pipe = dev.state(0), pipe.state(0)
+    np.testing.assert_array_equal(s_dev["origin"].cpu().numpy(), s_pipe["origin"].cpu().numpy())
+    np.testing.assert_array_equal(s_dev["mu"].cpu().numpy(), s_pipe["mu"].cpu().numpy())
