@@ -22,6 +22,8 @@
 #include "common.cuh"
 #include "tc_util.cuh"
 
+#include <type_traits>
+
 namespace cascade {
 
 namespace {
@@ -186,23 +188,58 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         const int k0 = (j - p.n_res_tiles) * 128;
         lim = min(qi - k0 + 1, p.m - k0);
       }
-      // row max over raw S (scale > 0), masking only on the (few) partial tiles
-      float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-      if (lim < 128) {
+      if (lim < 128) {                                    // mask only the (few) partial tiles
 #pragma unroll
         for (int c = 0; c < 128; ++c) x[c] = c < lim ? x[c] : -INFINITY;
       }
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      // exp2 of the tile against row offset mu -> P (bf16, TMEM) and its row sum; with TRACK,
+      // the raw tile max is reduced alongside (ALU pipe, next to the MUFU / FMA work)
+      auto exp_pass = [&](float mu, float& mraw, auto track) -> float {
+        const float2 nm2 = make_float2(-mu, -mu);
+        float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+        float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; c += 4) {
-        m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
-      }
-      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * p.scale_log2;
+        for (int c = 0; c < 4; ++c) {                     // 32 keys -> 16 packed columns per store
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float xa = x[c * 32 + 2 * e], xb = x[c * 32 + 2 * e + 1];
+            if (decltype(track)::value) { m0 = fmaxf(m0, xa); m1 = fmaxf(m1, xb); }
+            const float2 t = __ffma2_rn(make_float2(xa, xb), sc2, nm2);
+            // EMU of every 16 pairs on the FMA pipe (degree-3 polynomial; P is rounded to bf16
+            // anyway), the rest on MUFU
+            const bool emu = ((e * EMU) % 16) + EMU >= 16;
+            const float2 pp = emu ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
+            if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
+            pk[e] = tc::pack_bf16(pp.x, pp.y);
+          }
+          tc::tmem_st16(sb + 64 + c * 16, pk);
+        }
+        if (decltype(track)::value) mraw = fmaxf(m0, m1);
+        const float2 s01 = __fadd2_rn(s0, s1);
+        return s01.x + s01.y;
+      };
+      using Track = std::integral_constant<bool, true>;
+      using NoTrack = std::integral_constant<bool, false>;
+      float mraw = -INFINITY;
       if (j == 0) {
-        m_used = mx;
+        // first tile: the row max first
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
+        }
+        m_used = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * p.scale_log2;
+        l += exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, NoTrack{});
       } else {
-        // Lazy rescale of the O row when its max grew by more than 2^8.  tcgen05.ld/st are
+        // later tiles: exp2 against the running max right away (P may reach 2^8 before a lazy
+        // rescale, fine in fp32 / bf16); the tile max comes with it, and only if it grew by
+        // more than 2^8 (rare) is O rescaled and the tile redone.  tcgen05.ld/st are
         // warp-collective, so the whole warp takes the branch if any row needs it; O must
         // hold every PV up to tile j-1 first.
+        const float sum = exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, Track{});
+        const float mx = mraw * p.scale_log2;
         const bool need = mx > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
           tc::mbar_wait(pv_done, (j - 1) & 1);
@@ -218,34 +255,21 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             tc::tmem_st32(tmem + kColO + lane_off + c * 32, o);
           }
           if (need) { l *= f; m_used = mx; }
+          tc::tmem_wait_st();                             // the first pass's P stores land first
+          l += exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, NoTrack{});
+        } else {
+          l += sum;
         }
       }
-      const float mu = m_used == -INFINITY ? 0.f : m_used;
-      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-mu, -mu);
-      float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {                       // 32 keys -> 16 packed columns per store
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float2 t = __ffma2_rn(make_float2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sc2, nm2);
-          // EMU of every 16 pairs on the FMA pipe (degree-3 polynomial; P is rounded to bf16
-          // anyway), the rest on MUFU
-          const bool emu = ((e * EMU) % 16) + EMU >= 16;
-          const float2 pp = emu ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
-          if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
-          pk[e] = tc::pack_bf16(pp.x, pp.y);
-        }
-        tc::tmem_st16(sb + 64 + c * 16, pk);
-      }
-      const float2 s01 = __fadd2_rn(s0, s1);
-      l += s01.x + s01.y;
       tc::tmem_wait_st();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
     }
-    // epilogue
+    // epilogue.  pv_done completes once per PV; when the last P is written only PV(nt-3) is
+    // known complete (QK(nt-1) followed it), so a parity wait for phase nt-1 alone could be
+    // satisfied by phase nt-3: wait for nt-2 first, then nt-1.
+    if (nt >= 2) tc::mbar_wait(pv_done, (nt - 2) & 1);
     tc::mbar_wait(pv_done, (nt - 1) & 1);
     tc::tc_fence_after();
     const float inv = 1.f / l;
