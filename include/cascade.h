@@ -92,8 +92,11 @@ typedef struct {
   double rope_theta;     /* RoPE base > 0 (Q11)                                 */
   double softmax_scale;  /* 0 -> 1/sqrt(d) (Eq. 1)                              */
   int32_t head_policy;   /* 0 = independent heads; others unsupported   */
-  int32_t head_reduce;   /* 0 = max over the GQA group; others unsupp.  */
-  int32_t selection;     /* 1 = EMA token selection; 0 unsupported      */
+  int32_t head_reduce;   /* 0 = max over the GQA group; 1 = mean (the   */
+                         /* head-reduction ablation); else CONFIG       */
+  int32_t selection;     /* 1 = EMA token selection; 0 = the ablation   */
+                         /* without it (reading Q3: the resident stays and the */
+                         /* carried token is dropped); else CONFIG      */
   int32_t reserved;
 } cascade_config;
 

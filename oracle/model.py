@@ -7,7 +7,8 @@ Per call, for one layer (Alg. 1; cache.get -> layer -> cache.u
  2. RoPE by pe on cached keys, chunk keys and chunk queries (Q11).
  3. For every q-head h of kv-group g = h // G: exact chunk attention (Eq. 1/2,
     Fig. 4 slice) and its per-key EMA mass s_h (Alg. 3, exact normaliser, Q6).
- 4. s_g = max_h s_h over the group (independent heads + max, Q7).
+ 4. s_g = max_h s_h over the group (independent heads + max, Q7); the head-reduction
+    ablation takes the mean instead (``head_reduce``).
  5. Fold (P:154 over m rows, Q4): residents mu <- gamma**m * mu + s_g;
     chunk tokens start at mu = 0, so mu = s_g (Q8).  All folds happen before
     any insertion (Q9).
@@ -43,7 +44,8 @@ class OracleConfig:
     gamma: float = 0.9999
     rope_theta: float = 10000.0
     softmax_scale: float = 0.0        # 0 -> 1/sqrt(d)
-    selection: bool = True
+    selection: bool = True            # False: the ablation without token selection (Q3)
+    head_reduce: str = "max"          # GQA reduction of s: "max" (the paper's) or "mean"
     # Reading Q17: in the bf16 configs the rotated q and k are the operands the score
     # products consume, held in bf16 (the model dtype the paper's kernel runs in); the
     # oracle rounds them to bf16 (round-to-nearest-even) before its float64 dot products.
@@ -137,7 +139,7 @@ class CascadeOracle:
                     O[b, :, h] = o_h
                     s_h[j] = key_mass(P, cfg.gamma)
                     s_heads_out[b, h, key_slot] = s_h[j]
-                s_g = reduce_heads(s_h, G, "max")[0]
+                s_g = reduce_heads(s_h, G, cfg.head_reduce)[0]
                 s_out[b, g, key_slot] = s_g
                 self._fold_and_insert(head, k[b, :, g], v[b, :, g], s_out[b, g])
         if return_heads:

@@ -119,12 +119,15 @@ class CascadeConfig:
     ema_gamma: float = 0.9999
     rope_theta: float = 500000.0
     softmax_scale: float = 0.0
+    head_reduce: str = "max"      # "max" or "mean" (P:542 ablation)
+    selection: bool = True        # False: the ablation without token selection (Q3)
 
     def c_struct(self) -> _Config:
         return _Config(self.num_layers, self.batch, self.num_q_heads, self.num_kv_heads,
                        self.head_dim, self.sink_size, self.cache_size, self.num_cascades,
                        self.max_stride, BF16 if self.dtype == "bf16" else F32,
-                       self.ema_gamma, self.rope_theta, self.softmax_scale, 0, 0, 1, 0)
+                       self.ema_gamma, self.rope_theta, self.softmax_scale, 0,
+                       {"max": 0, "mean": 1}[self.head_reduce], int(self.selection), 0)
 
     @property
     def torch_dtype(self):

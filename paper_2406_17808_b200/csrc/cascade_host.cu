@@ -225,7 +225,9 @@ cascade_status cascade_validate_config(const cascade_config* c) {
   if (!(c->rope_theta > 0.0) || c->softmax_scale < 0.0) return CASCADE_ERR_CONFIG;
   if (c->max_stride < 1) return CASCADE_ERR_CONFIG;
   if (c->dtype != CASCADE_F32 && c->dtype != CASCADE_BF16) return CASCADE_ERR_CONFIG;
-  if (c->head_policy != 0 || c->head_reduce != 0 || c->selection != 1) return CASCADE_ERR_UNSUPPORTED;
+  if (c->selection != 0 && c->selection != 1) return CASCADE_ERR_CONFIG;
+  if (c->head_reduce != 0 && c->head_reduce != 1) return CASCADE_ERR_CONFIG;
+  if (c->head_policy != 0) return CASCADE_ERR_UNSUPPORTED;
   const long long S = (long long)c->sink_size + c->cache_size;
   if (S + c->max_stride > (1LL << 30)) return CASCADE_ERR_CONFIG;
   return CASCADE_OK;
@@ -244,7 +246,7 @@ cascade_status cascade_mirror_advance(const cascade_config* cfg, cascade_mirror*
   if (m < 0) return CASCADE_ERR_SHAPE;
   const int32_t N = cfg->num_cascades, c = cfg->cache_size / N;
   Planner p;
-  p.configure(cfg->sink_size, N, c);
+  p.configure(cfg->sink_size, N, c, cfg->selection != 0);
   Plan plan;
   p.advance(*mirror, m, ops_out ? &plan : nullptr);
   if (pe_out) mirror_positions(*mirror, cfg->sink_size, N, c, pe_out);
@@ -295,7 +297,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->N = cfg->num_cascades;
   h->c = cfg->cache_size / cfg->num_cascades;
   h->S_tot = h->alpha + cfg->cache_size;
-  h->planner.configure(h->alpha, h->N, h->c);
+  h->planner.configure(h->alpha, h->N, h->c, h->cfg.selection != 0);
   h->launches = 0;
   h->ring_pos = 0;
   h->profiling = false;
@@ -425,6 +427,7 @@ Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_
   g.scale = (float)scale;
   g.scale_log2 = (float)(scale * 1.4426950408889634);
   g.decay = gamma_pow(c.ema_gamma, m);
+  g.head_mean = c.head_reduce == 1;
   return g;
 }
 
@@ -651,6 +654,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
     tp.q_rot = q_rot; tp.k_rot = k_rot; tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
     tp.mu = L.mu; tp.decay = g.decay;   // pass 2 folds the EMA in its epilogue
+    tp.head_mean = g.head_mean;
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);
@@ -795,6 +799,7 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   dp.scale_log2 = g.scale_log2;
   dp.w0 = (float)((1.0 - h->cfg.ema_gamma) * gamma_pow(h->cfg.ema_gamma, 0));
   dp.decay = g.decay;
+  dp.head_mean = g.head_mean;
   dp.q = static_cast<const __nv_bfloat16*>(q);
   dp.k_new = static_cast<const __nv_bfloat16*>(k);
   dp.v_new = static_cast<const __nv_bfloat16*>(v);

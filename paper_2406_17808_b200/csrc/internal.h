@@ -26,6 +26,7 @@ struct Geometry {
   float scale;                          // softmax scale
   float scale_log2;                     // scale * log2(e)
   double decay;                         // g = gamma^m
+  int32_t head_mean;                    // GQA head reduction of s: 0 max, 1 mean (P:542 ablation)
 };
 
 // pe of a pre-chunk resident flat slot x (-1 if empty).  Closed form of the logical
@@ -127,6 +128,7 @@ struct TcParams {
   float* s;                     // [B*Hkv][S_tot + m]
   double* mu;                   // [B*Hkv][S_tot] EMA state: pass 2 folds mu <- decay*mu + s
   double decay;                 // gamma^m
+  int32_t head_mean;            // 0: s_g = max over the group; 1: the mean (P:542 ablation)
 };
 // single-token decode (k_decode.cu)
 struct DecodeParams {
@@ -141,6 +143,7 @@ struct DecodeParams {
   float scale_log2;             // softmax scale * log2(e)
   float w0;                     // (1 - gamma): EMA weight of the single row (Alg. 3, m = 1)
   double decay;                 // gamma
+  int32_t head_mean;            // 0: max over the group; 1: mean (P:542 ablation)
   const __nv_bfloat16* q;       // [B][Hq][D]   pre-RoPE
   const __nv_bfloat16* k_new;   // [B][Hkv][D]
   const __nv_bfloat16* v_new;   // [B][Hkv][D]

@@ -106,8 +106,9 @@ __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
       float logit = warp_sum(part) * g.scale;
       acc += w[r] * expf(logit - lb[r]);
     }
-    best = j == 0 ? acc : fmaxf(best, acc);
+    best = j == 0 ? acc : (g.head_mean ? best + acc : fmaxf(best, acc));   // P:542 (max; mean ablation)
   }
+  if (g.head_mean) best = __fdiv_rn(best, (float)g.G);
   if (lane == 0) s[warp] = best;
 }
 

@@ -506,7 +506,12 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       const float* h0 = sacc + (wg * 2 + 0) * p.G * 128;
       const float* h1 = sacc + (wg * 2 + 1) * p.G * 128;
       float best = 0.f;
-      for (int hh = 0; hh < p.G; ++hh) best = fmaxf(best, h0[hh * 128 + r] + h1[hh * 128 + r]);
+      if (p.head_mean) {                                  // mean over the group (P:542 ablation)
+        for (int hh = 0; hh < p.G; ++hh) best += h0[hh * 128 + r] + h1[hh * 128 + r];
+        best = __fdiv_rn(best, (float)p.G);
+      } else {                                            // max over the group
+        for (int hh = 0; hh < p.G; ++hh) best = fmaxf(best, h0[hh * 128 + r] + h1[hh * 128 + r]);
+      }
       p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
       if (resident)                                       // EMA fold (Q4), never an FMA
         p.mu[bg * p.S_tot + kstart + r] = __dadd_rn(__dmul_rn(p.decay, smu[wg * 128 + r]), (double)best);

@@ -454,7 +454,10 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
       const int x = beg + o;
       if (o >= len) { s_out[x] = 0.f; continue; }
       float best = 0.f;
-      if (p.G == 4) {
+      if (p.head_mean) {                                   // mean over the group (P:542 ablation)
+        for (int h = 0; h < p.G; ++h) best += exp2f(lg[(long long)x * p.G + h] - sl[h]);
+        best = __fdiv_rn(best, (float)p.G);
+      } else if (p.G == 4) {
         const float4 l = lg4[x];
         best = fmaxf(fmaxf(exp2f(l.x - sl[0]), exp2f(l.y - sl[1])), fmaxf(exp2f(l.z - sl[2]), exp2f(l.w - sl[3])));
       } else {
@@ -467,7 +470,11 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
   }
   if (tid == 0) {
     float best = 0.f;
-    for (int h = 0; h < p.G; ++h) best = fmaxf(best, exp2f(lg[(long long)p.S_tot * p.G + h] - sl[h]));
+    for (int h = 0; h < p.G; ++h) {
+      const float e = exp2f(lg[(long long)p.S_tot * p.G + h] - sl[h]);
+      best = p.head_mean ? best + e : fmaxf(best, e);
+    }
+    if (p.head_mean) best = __fdiv_rn(best, (float)p.G);
     s_out[p.S_tot] = p.w0 * best;
   }
   __syncthreads();

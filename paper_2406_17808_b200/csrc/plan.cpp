@@ -5,8 +5,9 @@
 
 namespace cascade {
 
-void Planner::configure(int32_t alpha, int32_t N, int32_t c) {
+void Planner::configure(int32_t alpha, int32_t N, int32_t c, bool selection) {
   alpha_ = alpha; N_ = N; c_ = c; S_tot_ = alpha + N * c;
+  selection_ = selection;
   occ_.assign(S_tot_, 0);
   stamp_.assign(S_tot_, 0);
   cur_ = 0;
@@ -45,6 +46,9 @@ void Planner::advance(cascade_mirror& mr, int32_t m, Plan* plan) {
         set(x, item);
         mr.xi[i] = (mr.xi[i] + 1) % c_;
         item = ev;
+      } else if (!selection_) {                       // ablation (Q3): resident stays, carried dropped
+        ++drops;
+        placed = true;
       } else {                                        // token selection vs newest
         const int32_t ns = base + (mr.xi[i] - 1 + c_) % c_;
         const int32_t inc = get(ns);

@@ -28,12 +28,15 @@ struct Plan {
 
 class Planner {
  public:
-  void configure(int32_t alpha, int32_t N, int32_t c);
+  // selection = false: the ablation without token selection (reading Q3: the resident stays,
+  // the carried token is dropped)
+  void configure(int32_t alpha, int32_t N, int32_t c, bool selection = true);
   // Advances `mr` by m insertions starting at stream index mr.t; fills plan if non-null.
   void advance(cascade_mirror& mr, int32_t m, Plan* plan);
 
  private:
   int32_t alpha_ = 0, N_ = 0, c_ = 0, S_tot_ = 0;
+  bool selection_ = true;
   std::vector<int32_t> occ_;
   std::vector<uint32_t> stamp_;
   std::vector<int32_t> touched_;

@@ -46,6 +46,18 @@ def test_config_validation(field, value, code):
     assert C.workspace_bytes(cfg) == 0
 
 
+def test_ablation_options_validate():
+    """head_reduce 0/1 (max, mean: P:542) and selection 0/1 (Q3) are accepted; other values are
+    CONFIG errors; the homogeneous head policy is not implemented (UNSUPPORTED)."""
+    import ctypes
+    L = C.lib()
+    assert C.validate(C.CascadeConfig(head_reduce="mean", selection=False)) == 0
+    for field, value, code in [("head_reduce", 2, -2), ("selection", 2, -2), ("head_policy", 1, -7)]:
+        st = C.CascadeConfig().c_struct()
+        setattr(st, field, value)
+        assert L.cascade_validate_config(ctypes.byref(st)) == code
+
+
 def test_workspace_bytes_grow_with_layers():
     a = C.workspace_bytes(C.CascadeConfig(num_layers=1))
     b = C.workspace_bytes(C.CascadeConfig(num_layers=2))
@@ -70,9 +82,11 @@ def test_host_mirror_matches_oracle_counters_and_positions():
         N = int(rng.integers(1, 6))
         c = int(rng.integers(1, 9))
         alpha = int(rng.integers(0, 6))
-        cfg = C.CascadeConfig(sink_size=alpha, cache_size=N * c, num_cascades=N, max_stride=64)
+        sel = bool(rng.random() < 0.7)
+        cfg = C.CascadeConfig(sink_size=alpha, cache_size=N * c, num_cascades=N, max_stride=64,
+                              selection=sel)
         mirror = C.Mirror()
-        head = CascadeHead(alpha, N * c, N)
+        head = CascadeHead(alpha, N * c, N, selection=sel)
         T = 0
         for _ in range(int(rng.integers(1, 12))):
             m = int(rng.integers(1, 40))
@@ -89,6 +103,8 @@ def test_host_mirror_matches_oracle_counters_and_positions():
             np.testing.assert_array_equal(pe, _oracle_pe(head, alpha, N, c))
             assert ops[2] == drops
             assert ops[3] in (0, 1) or m > c       # selections of a chunk are independent unless m > c
+            if not sel:
+                assert ops[0] == 0 and ops[3] == 0  # no selection: nothing to resolve on the device
 
 
 def test_cfg3_schedule_is_depth_zero_and_fill_trajectory():

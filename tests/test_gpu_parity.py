@@ -29,7 +29,8 @@ def _np(t):
 def _oracle_cfg(cfg: C.CascadeConfig) -> OracleConfig:
     return OracleConfig(cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
                         cfg.sink_size, cfg.cache_size, cfg.num_cascades, gamma=cfg.ema_gamma,
-                        rope_theta=cfg.rope_theta, round_operands="bf16" if cfg.dtype == "bf16" else "")
+                        rope_theta=cfg.rope_theta, round_operands="bf16" if cfg.dtype == "bf16" else "",
+                        selection=cfg.selection, head_reduce=cfg.head_reduce)
 
 
 def _compare_state(gpu_state, orc_state, exact_mu=True, exact_payload=True, layer_meta=None):
@@ -63,10 +64,10 @@ SMALL = [  # (alpha, N, c, B, Hkv, dtype, strides)
 
 
 @pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", SMALL)
-def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=64):
+def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=64, selection=True):
     cfg = C.CascadeConfig(batch=B, num_q_heads=Hkv, num_kv_heads=Hkv, head_dim=d, sink_size=alpha,
                           cache_size=N * c, num_cascades=N, max_stride=max(strides), dtype=dtype,
-                          ema_gamma=0.99)
+                          ema_gamma=0.99, selection=selection)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))
     rng = np.random.default_rng(alpha * 131 + N * 17 + c)
@@ -96,6 +97,12 @@ MULTI_ROUND = [
 @pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", MULTI_ROUND)
 def test_score_injection_multi_round_maintenance(alpha, N, c, B, Hkv, dtype, strides):
     test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=128)
+
+
+@pytest.mark.parametrize("idx", [0, 2, 4, 5])
+def test_score_injection_selection_off_bit_exact(idx):
+    """The ablation without token selection (reading Q3): same bit-exact bar."""
+    test_score_injection_state_bit_exact(*SMALL[idx], selection=False)
 
 
 def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_advance=0):
@@ -180,6 +187,43 @@ def test_decode_matches_oracle():
         assert np.abs(_np(out) - O_ref).max() <= O_TOL["bf16"]
         np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
     _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
+
+
+@pytest.mark.parametrize("dtype,head_reduce,selection", [("bf16", "mean", True), ("f32", "mean", True),
+                                                       ("bf16", "max", False)])
+def test_ablation_variants_end_to_end(dtype, head_reduce, selection):
+    """The paper's ablations through both prefill paths and decode: the mean head reduction
+     and no token selection (Q3), GQA 4:1, B = 2, ragged last chunk."""
+    d = 128 if dtype == "bf16" else 64
+    cfg = C.CascadeConfig(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=d, sink_size=4,
+                          cache_size=64, num_cascades=4, max_stride=48, dtype=dtype,
+                          head_reduce=head_reduce, selection=selection)
+    syn = Synth(2, 8, 2, d, seed=1234, dtype=cfg.torch_dtype)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    start = 0
+    for m in [48, 48, 48, 48, 31]:
+        q, k, v = syn.chunk(start, m)
+        start += m
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        O_ref, s_ref = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL[dtype]
+        np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+        _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
+    if dtype == "bf16":
+        for step in range(12):
+            q, k, v = syn.chunk(start + step, 1)
+            out = gpu.decode(0, q[:, 0].contiguous().cuda(), k[:, 0].contiguous().cuda(),
+                             v[:, 0].contiguous().cuda())
+            O_ref, s_ref = orc.decode(0, _np(q[:, 0]), _np(k[:, 0]), _np(v[:, 0]))
+            torch.cuda.synchronize()
+            assert np.abs(_np(out) - O_ref).max() <= O_TOL["bf16"]
+            np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+        _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
+    if selection:                    # margin audit; without selection mu decides nothing
+        margins = orc.select_margins()
+        assert margins.size > 0 and margins.min() > 1e-3, margins.min()
 
 
 def test_errors_leave_state_untouched():

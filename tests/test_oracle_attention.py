@@ -264,3 +264,29 @@ def test_slice_rows_equals_chunk_attention_rows():
     o2, P2 = slice_rows(q[rows], rows, k, v, n_c, 0.3)
     np.testing.assert_array_equal(P2, P[rows])
     np.testing.assert_allclose(o2, o[rows], rtol=0, atol=1e-15)
+
+
+def test_mean_head_reduction_keeps_the_sum_rule():
+    """Head-reduction ablation: with the mean over the GQA group every kv-head's
+    scores of a chunk still sum to 1 - gamma^m (each head's do, Alg. 3), while the max
+    sums to at least that; with one q-head per kv-head both reductions are the identity."""
+    rng = np.random.default_rng(17)
+    m, d, gam = 24, 16, 0.99
+    q, k, v = _toy_inputs(1, m, 4, 1, d, 3)
+    for how in ("mean", "max"):
+        orc = CascadeOracle(OracleConfig(num_layers=1, batch=1, num_q_heads=4, num_kv_heads=1,
+                                         head_dim=d, sink_size=2, cache_size=8, num_cascades=2,
+                                         gamma=gam, head_reduce=how))
+        _, s = orc.prefill_stride(0, q, k, v)
+        if how == "mean":
+            assert s[0, 0].sum() == pytest.approx(1 - gam ** m, rel=1e-12)
+        else:
+            assert s[0, 0].sum() > 1 - gam ** m
+    q1, k1, v1 = (rng.standard_normal((1, m, 2, d)) for _ in range(3))
+    outs = []
+    for how in ("mean", "max"):
+        orc = CascadeOracle(OracleConfig(num_layers=1, batch=1, num_q_heads=2, num_kv_heads=2,
+                                         head_dim=d, sink_size=2, cache_size=8, num_cascades=2,
+                                         gamma=gam, head_reduce=how))
+        outs.append(orc.prefill_stride(0, q1, k1, v1)[1])
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -232,3 +232,39 @@ def test_ring_push_and_replace_semantics():
     r.replace_newest(Token(3))
     assert [t.origin for t in r.oldest_to_newest()] == [1, 3]
     assert r.push(Token(4)).origin == 1 and r.push(Token(5)).origin == 3
+
+
+def test_selection_off_is_keep_resident_and_scores_irrelevant():
+    """Reading Q3 ("w/o token selection"): the resident stays and the carried token is
+    dropped, i.e. the cascade behaves as under score selection with all scores equal (strict
+    '>' never fires, Q2).  Pinned three ways on random streams: (1) contents equal those of a
+    selection-on cascade fed equal scores, (2) the ring model equals the shifting-list model
+    with selection off, (3) the span stays in the keep-resident band [S~ - (2^(N-1) - 1), S~]
+    of SURVEY App. B.2 (Eq. 4)."""
+    rng = np.random.default_rng(99)
+    for _ in range(300):
+        N = int(rng.integers(1, 5))
+        c = int(rng.integers(1, 5))
+        alpha = int(rng.integers(0, 4))
+        T = int(rng.integers(1, 80))
+        off = CascadeHead(alpha, N * c, N, selection=False)
+        tied = CascadeHead(alpha, N * c, N)
+        naive = NaiveCascade(alpha, N * c, N, selection=False)
+        for t in range(T):
+            mu = float(rng.random())
+            off.add_token(Token(origin=t, mu=mu))
+            tied.add_token(Token(origin=t, mu=0.25))
+            naive.add(t, mu)
+            got = [o for o, _ in off.positions()]
+            assert got == [o for o, _ in tied.positions()]
+            assert got == naive.logical_origins()
+    for C, N in [(8, 4), (64, 4), (40, 2), (64, 8)]:
+        head = CascadeHead(0, C, N, selection=False)
+        S_tilde = token_span(C, N)
+        spans = []
+        for t in range(6 * S_tilde + 200):
+            head.add_token(Token(origin=t, mu=float(rng.random())))
+            if t > 4 * S_tilde:
+                o = [x for x, _ in head.positions()]
+                spans.append(o[-1] - o[0] + 1)
+        assert max(spans) == S_tilde and min(spans) >= S_tilde - (2 ** (N - 1) - 1)
