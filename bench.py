@@ -380,7 +380,10 @@ def main():
                                   "the EMA fold runs in attn_score's epilogue)",
                         "bound": "hbm", "achieved": rm / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": rm / 1e9 / peaks["hbm"],
-                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)"},
+                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)",
+                        "note": "event-timed per launch: includes ~5 us of launch + event edge per launch "
+                                "(profiles/launch_edge_r01.txt); the kernel's own span streams at ~69 % "
+                                "(DESIGN.md, Cache maintenance)"},
     }
     share = {k: v["ms_per_step"] / ms_step for k, v in kern.items()}
 
