@@ -91,9 +91,15 @@ typedef struct {
   double ema_gamma;      /* gamma in [0,1] (0.9999 in the paper)  */
   double rope_theta;     /* RoPE base > 0 (Q11)                                 */
   double softmax_scale;  /* 0 -> 1/sqrt(d) (Eq. 1)                              */
-  int32_t head_policy;   /* 0 = independent heads; others unsupported   */
-  int32_t head_reduce;   /* 0 = max over the GQA group; 1 = mean (the   */
-                         /* head-reduction ablation); else CONFIG       */
+  int32_t head_policy;   /* 0 = independent heads (the paper's choice);  */
+                         /* 1 = homogeneous: s reduced over all kv-heads of a   */
+                         /* sequence, one decision for all (P:542 ablation;    */
+                         /* needs the unsharded head set; with head_reduce 2   */
+                         /* UNSUPPORTED); other values CONFIG                  */
+  int32_t head_reduce;   /* 0 = max over the GQA group; the ablations   */
+                         /* of P:542: 1 = mean, 2 = median (even group: mean   */
+                         /* of the middle two); 1/2 need Hq/Hkv <= 32 (else    */
+                         /* UNSUPPORTED); other values CONFIG                  */
   int32_t selection;     /* 1 = EMA token selection; 0 = the ablation   */
                          /* without it (reading Q3: the resident stays and the */
                          /* carried token is dropped); else CONFIG      */

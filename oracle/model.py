@@ -8,7 +8,8 @@ Per call, for one layer (Alg. 1; cache.get -> layer -> cache.u
  3. For every q-head h of kv-group g = h // G: exact chunk attention (Eq. 1/2,
     Fig. 4 slice) and its per-key EMA mass s_h (Alg. 3, exact normaliser, Q6).
  4. s_g = max_h s_h over the group (independent heads + max, Q7); the head-reduction
-    ablation takes the mean instead (``head_reduce``).
+    ablation takes the mean or the median instead (``head_reduce``); the homogeneous
+    head policy reduces over all q-heads of the sequence instead (``head_policy``).
  5. Fold (P:154 over m rows, Q4): residents mu <- gamma**m * mu + s_g;
     chunk tokens start at mu = 0, so mu = s_g (Q8).  All folds happen before
     any insertion (Q9).
@@ -45,7 +46,11 @@ class OracleConfig:
     rope_theta: float = 10000.0
     softmax_scale: float = 0.0        # 0 -> 1/sqrt(d)
     selection: bool = True            # False: the ablation without token selection (Q3)
-    head_reduce: str = "max"          # GQA reduction of s: "max" (the paper's) or "mean"
+    head_reduce: str = "max"          # GQA reduction of s: "max" (the paper's), "mean", "median"
+    # head policy: "independent" (each kv-head's cascade decides on its group's s_g, the
+    # paper's choice) or "homogeneous" (one decision per sequence: s reduced over ALL q-heads
+    # and applied to every kv-head, whose cascades then hold the same tokens)
+    head_policy: str = "independent"
     # Reading Q17: in the bf16 configs the rotated q and k are the operands the score
     # products consume, held in bf16 (the model dtype the paper's kernel runs in); the
     # oracle rounds them to bf16 (round-to-nearest-even) before its float64 dot products.
@@ -141,7 +146,12 @@ class CascadeOracle:
                     s_heads_out[b, h, key_slot] = s_h[j]
                 s_g = reduce_heads(s_h, G, cfg.head_reduce)[0]
                 s_out[b, g, key_slot] = s_g
-                self._fold_and_insert(head, k[b, :, g], v[b, :, g], s_out[b, g])
+            if cfg.head_policy == "homogeneous":            # one s per sequence
+                s_out[b, :] = reduce_heads(s_heads_out[b], Hq, cfg.head_reduce)[0]
+            elif cfg.head_policy != "independent":
+                raise ValueError(cfg.head_policy)
+            for g in range(cfg.num_kv_heads):               # heads' attention all used the pre-chunk state
+                self._fold_and_insert(self.heads[layer][b][g], k[b, :, g], v[b, :, g], s_out[b, g])
         if return_heads:
             return O, s_out, s_heads_out
         return O, s_out
@@ -154,10 +164,13 @@ class CascadeOracle:
     def update_with_scores(self, layer: int, k: np.ndarray, v: np.ndarray, s_flat: np.ndarray) -> None:
         """Score injection: fold the given s [B,Hkv,S_tot+m] and insert k/v [B,m,Hkv,d]."""
         cfg = self.cfg
+        s_flat = np.asarray(s_flat, dtype=np.float64)
         for b in range(cfg.batch):
+            s_b = s_flat[b]
+            if cfg.head_policy == "homogeneous":            # the kv-heads' s reduced per sequence
+                s_b = np.broadcast_to(reduce_heads(s_b, cfg.num_kv_heads, cfg.head_reduce), s_b.shape)
             for g in range(cfg.num_kv_heads):
-                self._fold_and_insert(self.heads[layer][b][g], k[b, :, g], v[b, :, g],
-                                      np.asarray(s_flat[b, g], dtype=np.float64))
+                self._fold_and_insert(self.heads[layer][b][g], k[b, :, g], v[b, :, g], s_b[g])
 
     def state(self, layer: int) -> dict:
         """Flat-slot export of every (b, g) cascade of a layer."""

@@ -226,8 +226,10 @@ cascade_status cascade_validate_config(const cascade_config* c) {
   if (c->max_stride < 1) return CASCADE_ERR_CONFIG;
   if (c->dtype != CASCADE_F32 && c->dtype != CASCADE_BF16) return CASCADE_ERR_CONFIG;
   if (c->selection != 0 && c->selection != 1) return CASCADE_ERR_CONFIG;
-  if (c->head_reduce != 0 && c->head_reduce != 1) return CASCADE_ERR_CONFIG;
-  if (c->head_policy != 0) return CASCADE_ERR_UNSUPPORTED;
+  if (c->head_reduce < 0 || c->head_reduce > 2) return CASCADE_ERR_CONFIG;
+  if (c->head_reduce != 0 && c->num_q_heads / c->num_kv_heads > 32) return CASCADE_ERR_UNSUPPORTED;
+  if (c->head_policy < 0 || c->head_policy > 1) return CASCADE_ERR_CONFIG;
+  if (c->head_policy == 1 && c->head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;  // median of all heads
   const long long S = (long long)c->sink_size + c->cache_size;
   if (S + c->max_stride > (1LL << 30)) return CASCADE_ERR_CONFIG;
   return CASCADE_OK;
@@ -427,7 +429,8 @@ Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_
   g.scale = (float)scale;
   g.scale_log2 = (float)(scale * 1.4426950408889634);
   g.decay = gamma_pow(c.ema_gamma, m);
-  g.head_mean = c.head_reduce == 1;
+  g.head_reduce = c.head_reduce;
+  g.homogeneous = c.head_policy == 1;
   return g;
 }
 
@@ -653,8 +656,9 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     tp.scale_log2 = g.scale_log2;
     tp.n_res_tiles = up.n_tiles; tp.res_tiles = up.tiles;
     tp.q_rot = q_rot; tp.k_rot = k_rot; tp.out = out; tp.qbias = L.lse; tp.log2w = up.log2w; tp.s = L.s;
-    tp.mu = L.mu; tp.decay = g.decay;   // pass 2 folds the EMA in its epilogue
-    tp.head_mean = g.head_mean;
+    tp.mu = g.homogeneous ? nullptr : L.mu;   // pass 2 folds the EMA in its epilogue
+    tp.decay = g.decay;
+    tp.head_reduce = g.head_reduce;
     cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
     {
       ProfScope ps(h, 1, st);
@@ -679,7 +683,12 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     }
   }
   h->launches += 3;
-  launch_maintenance<T>(h, g, L, up, k, v, L.s, /*folded=*/std::is_same<T, __nv_bfloat16>::value, st);
+  if (g.homogeneous) {        // one s per sequence, folded by the maintenance launch
+    launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
+    ++h->launches;
+  }
+  launch_maintenance<T>(h, g, L, up, k, v, L.s,
+                        /*folded=*/std::is_same<T, __nv_bfloat16>::value && !g.homogeneous, st);
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;   // commit the mirror
   h->m_last[layer] = m;
@@ -799,7 +808,8 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   dp.scale_log2 = g.scale_log2;
   dp.w0 = (float)((1.0 - h->cfg.ema_gamma) * gamma_pow(h->cfg.ema_gamma, 0));
   dp.decay = g.decay;
-  dp.head_mean = g.head_mean;
+  dp.head_reduce = g.head_reduce;
+  dp.homogeneous = g.homogeneous;
   dp.q = static_cast<const __nv_bfloat16*>(q);
   dp.k_new = static_cast<const __nv_bfloat16*>(k);
   dp.v_new = static_cast<const __nv_bfloat16*>(v);
@@ -820,7 +830,7 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
     // algorithmic bytes: K, V (2 d bf16) + logits (4 G) + mu r/w + s per key
     ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 4.0 * g.G + 16.0 + 4.0));
   }
-  h->launches += 3;
+  h->launches += g.homogeneous ? 5 : 3;
   if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
   h->mirrors[layer] = next;
   h->m_last[layer] = 1;
@@ -840,6 +850,13 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   rc = upload_plan(h, layer, m, st, &up, &next);
   if (rc != CASCADE_OK) return rc;
   const PlanDev& pd = up.pd;
+  if (g.homogeneous) {        // the injected kv-head scores reduced per sequence
+    const size_t n = (size_t)g.B * g.Hkv * (g.S_tot + m);
+    cudaMemcpyAsync(L.s, s, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
+    ++h->launches;
+    s = L.s;
+  }
   if (h->cfg.dtype == CASCADE_BF16)
     launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
                                       static_cast<const __nv_bfloat16*>(v), s, false, st);

@@ -32,6 +32,25 @@ __device__ __forceinline__ int resident_runs(const Geometry& g, int32_t* beg, in
   return n;
 }
 
+// Head-reduction ablations of s_g over the group's per-head masses v[0..G):
+// 1 = mean (summed in head order), 2 = median (even G: the mean of the two middle values, as
+// numpy's median).  Sorts v in place.  The default reduction, max, stays inline at each call site.
+constexpr int kMaxMedianGroup = 32;
+__device__ inline float group_reduce_ablation(float* v, int G, int mode) {
+  if (mode == 1) {
+    float sum = 0.f;
+    for (int i = 0; i < G; ++i) sum += v[i];
+    return __fdiv_rn(sum, (float)G);
+  }
+  for (int i = 1; i < G; ++i) {                    // insertion sort, G <= kMaxMedianGroup
+    const float x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) { v[j + 1] = v[j]; --j; }
+    v[j + 1] = x;
+  }
+  return (G & 1) ? v[G / 2] : __fdiv_rn(v[G / 2 - 1] + v[G / 2], 2.f);
+}
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace cascade

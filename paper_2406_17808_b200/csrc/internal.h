@@ -26,7 +26,8 @@ struct Geometry {
   float scale;                          // softmax scale
   float scale_log2;                     // scale * log2(e)
   double decay;                         // g = gamma^m
-  int32_t head_mean;                    // GQA head reduction of s: 0 max, 1 mean (P:542 ablation)
+  int32_t head_reduce;                  // GQA head reduction of s: 0 max; ablations 1 mean, 2 median
+  int32_t homogeneous;                  // head policy: 0 independent, 1 homogeneous
 };
 
 // pe of a pre-chunk resident flat slot x (-1 if empty).  Closed form of the logical
@@ -112,6 +113,10 @@ void launch_positions(const Geometry& g, int32_t* pe, cudaStream_t st);
 // folds in its epilogue.
 void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t st);
 
+// Homogeneous head policy: s[b][0..Hkv)[len] <- its reduction over the kv-heads
+// (mode 0 max, 1 mean), written back to every kv-head.
+void launch_head_homogenize(int B, int Hkv, int len, int mode, float* s, cudaStream_t st);
+
 // tcgen05 attention (k_attn_tc.cu)
 struct TcParams {
   int32_t B, Hq, Hkv, G, m, M, S_tot;
@@ -128,7 +133,7 @@ struct TcParams {
   float* s;                     // [B*Hkv][S_tot + m]
   double* mu;                   // [B*Hkv][S_tot] EMA state: pass 2 folds mu <- decay*mu + s
   double decay;                 // gamma^m
-  int32_t head_mean;            // 0: s_g = max over the group; 1: the mean (P:542 ablation)
+  int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
 };
 // single-token decode (k_decode.cu)
 struct DecodeParams {
@@ -143,7 +148,10 @@ struct DecodeParams {
   float scale_log2;             // softmax scale * log2(e)
   float w0;                     // (1 - gamma): EMA weight of the single row (Alg. 3, m = 1)
   double decay;                 // gamma
-  int32_t head_mean;            // 0: max over the group; 1: mean (P:542 ablation)
+  int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
+  int32_t homogeneous;          // head policy: 0 independent, 1 homogeneous
+  int32_t update_stage;         // decode_update: 0 all; 1 scores only; 2 fold/select/move from s
+                                // (1 and 2 bracket the homogeneous-policy reduction; set by launch_decode)
   const __nv_bfloat16* q;       // [B][Hq][D]   pre-RoPE
   const __nv_bfloat16* k_new;   // [B][Hkv][D]
   const __nv_bfloat16* v_new;   // [B][Hkv][D]

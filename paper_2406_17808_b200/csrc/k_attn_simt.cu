@@ -94,6 +94,7 @@ __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
   for (int e = 0; e < E; ++e) kv[e] = to_f(kp[lane + 32 * e]);
 
   float best = 0.f;
+  float hv[kMaxMedianGroup];
   for (int j = 0; j < g.G; ++j) {
     const int h = gg * g.G + j;
     const T* qb = q_rot + ((long long)b * g.Hq + h) * g.ldc * D;
@@ -106,9 +107,10 @@ __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
       float logit = warp_sum(part) * g.scale;
       acc += w[r] * expf(logit - lb[r]);
     }
-    best = j == 0 ? acc : (g.head_mean ? best + acc : fmaxf(best, acc));   // P:542 (max; mean ablation)
+    best = j == 0 ? acc : fmaxf(best, acc);       // max over the group
+    if (j < kMaxMedianGroup) hv[j] = acc;         // G <= 32 whenever an ablation is on
   }
-  if (g.head_mean) best = __fdiv_rn(best, (float)g.G);
+  if (g.head_reduce) best = group_reduce_ablation(hv, g.G, g.head_reduce);   // mean / median
   if (lane == 0) s[warp] = best;
 }
 

@@ -447,7 +447,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   } else if (warp == 3) {
     // EMA operands (mu) of the resident key tiles, staged for the epilogue's fold so the
     // math warps neither wait on HBM at the end nor hold them in registers
-    if (resident) {
+    if (resident && p.mu) {                              // mu null: the fold runs after (homogeneous)
       for (int w = 0; w < n_here; ++w) {
         const int2 tl = p.res_tiles[first + w];
         for (int j = lane; j < tl.y; j += 32) smu[w * 128 + j] = p.mu[bg * p.S_tot + tl.x + j];
@@ -506,14 +506,15 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
       const float* h0 = sacc + (wg * 2 + 0) * p.G * 128;
       const float* h1 = sacc + (wg * 2 + 1) * p.G * 128;
       float best = 0.f;
-      if (p.head_mean) {                                  // mean over the group (P:542 ablation)
-        for (int hh = 0; hh < p.G; ++hh) best += h0[hh * 128 + r] + h1[hh * 128 + r];
-        best = __fdiv_rn(best, (float)p.G);
-      } else {                                            // max over the group
+      if (p.head_reduce == 0) {                           // max over the group
         for (int hh = 0; hh < p.G; ++hh) best = fmaxf(best, h0[hh * 128 + r] + h1[hh * 128 + r]);
+      } else {                                            // mean / median ablations
+        float hv[kMaxMedianGroup];
+        for (int hh = 0; hh < p.G; ++hh) hv[hh] = h0[hh * 128 + r] + h1[hh * 128 + r];
+        best = group_reduce_ablation(hv, p.G, p.head_reduce);
       }
       p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
-      if (resident)                                       // EMA fold (Q4), never an FMA
+      if (resident && p.mu)                               // EMA fold (Q4), never an FMA
         p.mu[bg * p.S_tot + kstart + r] = __dadd_rn(__dmul_rn(p.decay, smu[wg * 128 + r]), (double)best);
     }
   }

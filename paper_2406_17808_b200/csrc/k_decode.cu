@@ -453,10 +453,15 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
     for (int o = tid; o < cap; o += blockDim.x) {
       const int x = beg + o;
       if (o >= len) { s_out[x] = 0.f; continue; }
+      if (p.update_stage == 2) {                           // s already reduced (homogeneous)
+        mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)s_out[x]);
+        continue;
+      }
       float best = 0.f;
-      if (p.head_mean) {                                   // mean over the group (P:542 ablation)
-        for (int h = 0; h < p.G; ++h) best += exp2f(lg[(long long)x * p.G + h] - sl[h]);
-        best = __fdiv_rn(best, (float)p.G);
+      if (p.head_reduce) {                                 // mean / median ablations
+        float hv[kMaxMedianGroup];
+        for (int h = 0; h < p.G; ++h) hv[h] = exp2f(lg[(long long)x * p.G + h] - sl[h]);
+        best = group_reduce_ablation(hv, p.G, p.head_reduce);
       } else if (p.G == 4) {
         const float4 l = lg4[x];
         best = fmaxf(fmaxf(exp2f(l.x - sl[0]), exp2f(l.y - sl[1])), fmaxf(exp2f(l.z - sl[2]), exp2f(l.w - sl[3])));
@@ -465,18 +470,20 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
       }
       const float sv = p.w0 * best;
       s_out[x] = sv;
-      mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)sv);
+      if (p.update_stage == 0) mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)sv);
     }
   }
-  if (tid == 0) {
-    float best = 0.f;
+  if (tid == 0 && p.update_stage != 2) {
+    float best = 0.f, hv[kMaxMedianGroup];
     for (int h = 0; h < p.G; ++h) {
       const float e = exp2f(lg[(long long)p.S_tot * p.G + h] - sl[h]);
-      best = p.head_mean ? best + e : fmaxf(best, e);
+      if (h < kMaxMedianGroup) hv[h] = e;           // G <= 32 whenever an ablation is on
+      best = fmaxf(best, e);
     }
-    if (p.head_mean) best = __fdiv_rn(best, (float)p.G);
+    if (p.head_reduce) best = group_reduce_ablation(hv, p.G, p.head_reduce);
     s_out[p.S_tot] = p.w0 * best;
   }
+  if (p.update_stage == 1) return;                         // scores only (homogeneous, stage 1)
   __syncthreads();
   // 2. selections (depth order), 3. moves deepest sub-cache first -- one warp, sequential
   if (tid < 32) {
@@ -558,7 +565,18 @@ void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, cons
   else if (p.G == 2) launch_attn<2>(p, tk, tv, st);
   else launch_attn<8>(p, tk, tv, st);
   decode_combine_kernel<128><<<p.B * p.Hq, 128, 0, st>>>(p, out);
-  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
+  if (!p.homogeneous) {
+    decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
+    return;
+  }
+  // homogeneous head policy: every kv-head's s, then one reduction per sequence, then
+  // the fold / selections / moves from the reduced s
+  DecodeParams q = p;
+  q.update_stage = 1;
+  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(q, pl, n_sel, phase_begin_dev, n_phase);
+  launch_head_homogenize(p.B, p.Hkv, p.S_tot + 1, p.head_reduce, p.s, st);
+  q.update_stage = 2;
+  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(q, pl, n_sel, phase_begin_dev, n_phase);
 }
 
 }  // namespace cascade

@@ -72,6 +72,30 @@ void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t
   ema_fold_kernel<<<blocks, 256, 0, st>>>(g, mu, s);
 }
 
+// Homogeneous head policy: one decision per sequence.  Reduces each sequence's
+// kv-head scores s[b, 0..Hkv) (already reduced over each GQA group) to one row -- max, or the
+// mean of the group means (= the mean over all q-heads, the groups being equal) -- and writes it
+// back to every kv-head, so every kv-head folds the same mu and takes the same selections.
+__global__ void head_homogenize_kernel(int B, int Hkv, int len, int mode, float* __restrict__ s) {
+  const long long total = (long long)B * len;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / len;
+    const int x = (int)(i - b * len);
+    float* sb = s + b * Hkv * (long long)len + x;
+    float r = sb[0];
+    for (int g = 1; g < Hkv; ++g) r = mode == 1 ? r + sb[(long long)g * len] : fmaxf(r, sb[(long long)g * len]);
+    if (mode == 1) r = __fdiv_rn(r, (float)Hkv);
+    for (int g = 0; g < Hkv; ++g) sb[(long long)g * len] = r;
+  }
+}
+
+void launch_head_homogenize(int B, int Hkv, int len, int mode, float* s, cudaStream_t st) {
+  const long long total = (long long)B * len;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+  head_homogenize_kernel<<<blocks, 256, 0, st>>>(B, Hkv, len, mode, s);
+}
+
 __global__ void select_resolve_kernel(Geometry g, PlanDev p, int32_t begin, int32_t end,
                                       const double* __restrict__ mu, const float* __restrict__ s) {
   const int n = end - begin;

@@ -47,12 +47,17 @@ def test_config_validation(field, value, code):
 
 
 def test_ablation_options_validate():
-    """head_reduce 0/1 (max, mean: P:542) and selection 0/1 (Q3) are accepted; other values are
-    CONFIG errors; the homogeneous head policy is not implemented (UNSUPPORTED)."""
+    """head_reduce 0/1/2 (max, mean, median: P:542) and selection 0/1 (Q3) are accepted; others are
+    CONFIG errors; head_policy 0/1 (independent, homogeneous: P:542), except the median over all
+    heads of a sequence (UNSUPPORTED)."""
     import ctypes
     L = C.lib()
     assert C.validate(C.CascadeConfig(head_reduce="mean", selection=False)) == 0
-    for field, value, code in [("head_reduce", 2, -2), ("selection", 2, -2), ("head_policy", 1, -7)]:
+    assert C.validate(C.CascadeConfig(head_reduce="median")) == 0
+    assert C.validate(C.CascadeConfig(head_reduce="median", num_q_heads=33, num_kv_heads=1)) == -7
+    assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="mean")) == 0
+    assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="median")) == -7
+    for field, value, code in [("head_reduce", 3, -2), ("selection", 2, -2), ("head_policy", 2, -2)]:
         st = C.CascadeConfig().c_struct()
         setattr(st, field, value)
         assert L.cascade_validate_config(ctypes.byref(st)) == code

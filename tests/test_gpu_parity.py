@@ -30,7 +30,8 @@ def _oracle_cfg(cfg: C.CascadeConfig) -> OracleConfig:
     return OracleConfig(cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
                         cfg.sink_size, cfg.cache_size, cfg.num_cascades, gamma=cfg.ema_gamma,
                         rope_theta=cfg.rope_theta, round_operands="bf16" if cfg.dtype == "bf16" else "",
-                        selection=cfg.selection, head_reduce=cfg.head_reduce)
+                        selection=cfg.selection, head_reduce=cfg.head_reduce,
+                        head_policy=cfg.head_policy)
 
 
 def _compare_state(gpu_state, orc_state, exact_mu=True, exact_payload=True, layer_meta=None):
@@ -64,10 +65,11 @@ SMALL = [  # (alpha, N, c, B, Hkv, dtype, strides)
 
 
 @pytest.mark.parametrize("alpha,N,c,B,Hkv,dtype,strides", SMALL)
-def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=64, selection=True):
+def test_score_injection_state_bit_exact(alpha, N, c, B, Hkv, dtype, strides, d=64, selection=True,
+                                         head_policy="independent"):
     cfg = C.CascadeConfig(batch=B, num_q_heads=Hkv, num_kv_heads=Hkv, head_dim=d, sink_size=alpha,
                           cache_size=N * c, num_cascades=N, max_stride=max(strides), dtype=dtype,
-                          ema_gamma=0.99, selection=selection)
+                          ema_gamma=0.99, selection=selection, head_policy=head_policy)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))
     rng = np.random.default_rng(alpha * 131 + N * 17 + c)
@@ -103,6 +105,13 @@ def test_score_injection_multi_round_maintenance(alpha, N, c, B, Hkv, dtype, str
 def test_score_injection_selection_off_bit_exact(idx):
     """The ablation without token selection (reading Q3): same bit-exact bar."""
     test_score_injection_state_bit_exact(*SMALL[idx], selection=False)
+
+
+@pytest.mark.parametrize("idx", [2, 3, 5])
+def test_score_injection_homogeneous_bit_exact(idx):
+    """Homogeneous head policy: the injected kv-head scores reduced (max) per sequence,
+    one decision for all kv-heads; same bit-exact bar."""
+    test_score_injection_state_bit_exact(*SMALL[idx], head_policy="homogeneous")
 
 
 def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_advance=0):
@@ -189,15 +198,20 @@ def test_decode_matches_oracle():
     _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
 
 
-@pytest.mark.parametrize("dtype,head_reduce,selection", [("bf16", "mean", True), ("f32", "mean", True),
-                                                       ("bf16", "max", False)])
-def test_ablation_variants_end_to_end(dtype, head_reduce, selection):
-    """The paper's ablations through both prefill paths and decode: the mean head reduction
-     and no token selection (Q3), GQA 4:1, B = 2, ragged last chunk."""
+@pytest.mark.parametrize("dtype,head_reduce,selection,head_policy", [
+    ("bf16", "mean", True, "independent"), ("f32", "mean", True, "independent"),
+    ("bf16", "median", True, "independent"), ("f32", "median", True, "independent"),
+    ("bf16", "max", False, "independent"),
+    ("bf16", "max", True, "homogeneous"), ("f32", "max", True, "homogeneous"),
+    ("bf16", "mean", True, "homogeneous")])
+def test_ablation_variants_end_to_end(dtype, head_reduce, selection, head_policy):
+    """The paper's ablations through both prefill paths and decode: the mean and median head
+    reductions and the homogeneous head policy and no token selection (Q3),
+    GQA 4:1, B = 2, ragged last chunk."""
     d = 128 if dtype == "bf16" else 64
     cfg = C.CascadeConfig(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=d, sink_size=4,
                           cache_size=64, num_cascades=4, max_stride=48, dtype=dtype,
-                          head_reduce=head_reduce, selection=selection)
+                          head_reduce=head_reduce, selection=selection, head_policy=head_policy)
     syn = Synth(2, 8, 2, d, seed=1234, dtype=cfg.torch_dtype)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))

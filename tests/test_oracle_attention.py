@@ -269,7 +269,7 @@ def test_slice_rows_equals_chunk_attention_rows():
 def test_mean_head_reduction_keeps_the_sum_rule():
     """Head-reduction ablation: with the mean over the GQA group every kv-head's
     scores of a chunk still sum to 1 - gamma^m (each head's do, Alg. 3), while the max
-    sums to at least that; with one q-head per kv-head both reductions are the identity."""
+    sums to at least that; with one q-head per kv-head every reduction is the identity."""
     rng = np.random.default_rng(17)
     m, d, gam = 24, 16, 0.99
     q, k, v = _toy_inputs(1, m, 4, 1, d, 3)
@@ -284,9 +284,10 @@ def test_mean_head_reduction_keeps_the_sum_rule():
             assert s[0, 0].sum() > 1 - gam ** m
     q1, k1, v1 = (rng.standard_normal((1, m, 2, d)) for _ in range(3))
     outs = []
-    for how in ("mean", "max"):
+    for how in ("mean", "max", "median"):
         orc = CascadeOracle(OracleConfig(num_layers=1, batch=1, num_q_heads=2, num_kv_heads=2,
                                          head_dim=d, sink_size=2, cache_size=8, num_cascades=2,
                                          gamma=gam, head_reduce=how))
         outs.append(orc.prefill_stride(0, q1, k1, v1)[1])
     np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])

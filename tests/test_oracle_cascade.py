@@ -268,3 +268,38 @@ def test_selection_off_is_keep_resident_and_scores_irrelevant():
                 o = [x for x, _ in head.positions()]
                 spans.append(o[-1] - o[0] + 1)
         assert max(spans) == S_tilde and min(spans) >= S_tilde - (2 ** (N - 1) - 1)
+
+
+def test_homogeneous_head_policy():
+    """Homogeneous heads: one selection per sequence.  Pins: every kv-head's cascade
+    holds the same origins after every chunk; with one kv-head the policy is the independent
+    one; under max, each kv-head's s is the max over ALL q-heads, so it bounds every group's
+    own max; under mean, the sum rule 1 - gamma^m (Alg. 3) still holds."""
+    from oracle.attention import reduce_heads
+    rng = np.random.default_rng(21)
+    d, m = 16, 12
+    base = dict(num_layers=1, batch=2, head_dim=d, sink_size=2, cache_size=8, num_cascades=4,
+                gamma=0.9)
+    for how in ("max", "mean"):
+        hom = CascadeOracle(OracleConfig(num_q_heads=8, num_kv_heads=4, head_policy="homogeneous",
+                                         head_reduce=how, **base))
+        for _ in range(6):
+            q = rng.standard_normal((2, m, 8, d))
+            k, v = rng.standard_normal((2, m, 4, d)), rng.standard_normal((2, m, 4, d))
+            _, s, s_heads = hom.prefill_stride(0, q, k, v, return_heads=True)
+            st = hom.state(0)
+            for b in range(2):
+                assert all(np.array_equal(st["origin"][b, 0], st["origin"][b, g]) for g in range(4))
+                assert all(np.array_equal(s[b, 0], s[b, g]) for g in range(4))
+                if how == "max":
+                    assert np.all(s[b, 0] >= reduce_heads(s_heads[b], 2, "max") - 0)
+                else:
+                    assert s[b, 0].sum() == pytest.approx(1 - 0.9 ** m, rel=1e-12)
+    one = [CascadeOracle(OracleConfig(num_q_heads=3, num_kv_heads=1, head_policy=pol, **base))
+           for pol in ("homogeneous", "independent")]
+    for _ in range(5):
+        q = rng.standard_normal((2, m, 3, d))
+        k, v = rng.standard_normal((2, m, 1, d)), rng.standard_normal((2, m, 1, d))
+        outs = [o.prefill_stride(0, q, k, v) for o in one]
+        np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(one[0].state(0)["origin"], one[1].state(0)["origin"])
