@@ -335,3 +335,29 @@ def test_host_buffer_paths_match_device_path():
     s_dev, s_pipe = dev.state(0), pipe.state(0)
     np.testing.assert_array_equal(s_dev["origin"].cpu().numpy(), s_pipe["origin"].cpu().numpy())
     np.testing.assert_array_equal(s_dev["mu"].cpu().numpy(), s_pipe["mu"].cpu().numpy())
+
+
+@pytest.mark.parametrize("selection", [True, False])
+def test_window_span_within_eq4_band_on_gpu(selection):
+    """Eq. 4 through the CUDA path: once the cascade is full, the span of the
+    non-sink window (newest - oldest origin + 1) of every kv-head lies in
+    [S~ - 2(2^(N-1) - 1), S~] with token selection and [S~ - (2^(N-1) - 1), S~] without
+    (the oracle pins the same bands, test_oracle_cascade)."""
+    N, c = 4, 1024
+    cfg = C.CascadeConfig(batch=1, num_q_heads=8, num_kv_heads=2, head_dim=128, sink_size=64,
+                          cache_size=N * c, num_cascades=N, max_stride=1024, dtype="bf16",
+                          selection=selection)
+    syn = Synth(1, 8, 2, 128, seed=31, passkey_depth=20000)
+    gpu = C.Cascade(cfg)
+    S_tilde = c * (2 ** N - 1)
+    for start in range(0, 40960, 1024):
+        q, k, v = syn.chunk(start, 1024, device="cuda")
+        gpu.prefill_stride(0, q, k, v)
+        if start + 1024 < 2 * S_tilde:
+            continue                                   # window not at its steady span yet
+        org = gpu.state(0)["origin"].cpu().numpy()[0]
+        slack = (2 if selection else 1) * (2 ** (N - 1) - 1)
+        for g in range(2):
+            o = org[g, 64:]
+            span = int(o.max() - o.min() + 1)
+            assert S_tilde - slack <= span <= S_tilde, (start, g, span)
