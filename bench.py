@@ -361,7 +361,7 @@ def main():
     # the SUSTAINED bf16 figure (MEASURED_PEAKS.json bf16_tflops_sustained); burst reported beside
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01_v6.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01_v11.json")) as f:
             traffic = json.load(f)["attn_fwd"]["dram_bytes_per_launch"]
     except Exception:
         pass
@@ -369,7 +369,7 @@ def main():
             "achieved": r1 / 1e12, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
             "frac": r1 / 1e12 / peaks["bf16_sus"], "frac_of_burst": r1 / 1e12 / peaks["bf16"],
             "traffic": traffic, "traffic_note": "dram read+write bytes of one steady-state launch "
-            "(n_cached 62463), profiles/ncu_traffic_r01_v6.json",
+            "(n_cached 62463), profiles/ncu_traffic_r01_v11.json",
             "peak_source": peaks["src"] + " bf16 dense, sustained (kernel timed inside a long step)",
             "work": "4*d flops per visible (query, key) pair"}
     extra_roof = {
