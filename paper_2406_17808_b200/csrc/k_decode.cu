@@ -446,6 +446,37 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
   // 1. exact mass + fold for every valid slot, run by run (sinks, C_1 .. C_N); the new token's
   //    mass lands at S_tot.  Empty slots keep s = 0 (zeroed when the layer was reset / init).
   const float4* lg4 = reinterpret_cast<const float4*>(lg);
+  if (p.G == 4 && p.head_reduce == 0 && p.update_stage == 0) {
+    // the common case (GQA 4:1, max): kU slots per thread in flight -- every logit / mu load of
+    // the batch is issued before the first use, so the pass streams at HBM rate rather than at
+    // one load round trip per slot
+    constexpr int kU = 4;
+    for (int run = 0; run <= p.N; ++run) {
+      const int beg = run == 0 ? 0 : p.alpha + (run - 1) * p.c;
+      const int len = run == 0 ? p.sink_pre : p.counts[run - 1];
+      const int cap = run == 0 ? p.alpha : p.c;
+      for (int o0 = tid; o0 < cap; o0 += kU * blockDim.x) {
+        float4 l[kU];
+        double m[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int o = o0 + u * blockDim.x;
+          if (o < len) { l[u] = __ldcs(lg4 + beg + o); m[u] = mu[beg + o]; }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int o = o0 + u * blockDim.x, x = beg + o;
+          if (o >= cap) continue;
+          if (o >= len) { s_out[x] = 0.f; continue; }
+          const float best = fmaxf(fmaxf(exp2f(l[u].x - sl[0]), exp2f(l[u].y - sl[1])),
+                                   fmaxf(exp2f(l[u].z - sl[2]), exp2f(l[u].w - sl[3])));
+          const float sv = p.w0 * best;
+          s_out[x] = sv;
+          mu[x] = __dadd_rn(__dmul_rn(p.decay, m[u]), (double)sv);
+        }
+      }
+    }
+  } else
   for (int run = 0; run <= p.N; ++run) {
     const int beg = run == 0 ? 0 : p.alpha + (run - 1) * p.c;
     const int len = run == 0 ? p.sink_pre : p.counts[run - 1];
