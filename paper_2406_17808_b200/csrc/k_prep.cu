@@ -69,28 +69,30 @@ __device__ __forceinline__ void rotate(uint4& lo, uint4& hi, const float2* __res
 
 }  // namespace
 
-template <typename T>
+// I: index type of the task / row arithmetic -- 32-bit whenever the task count fits (the
+// divisions by Hq, S_tot + m, Hkv and m are then 32-bit, a fraction of the 64-bit cost)
+template <typename T, typename I>
 __global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* __restrict__ k,
                                                         const T* __restrict__ v, const T* __restrict__ k_raw,
                                                         const float2* __restrict__ tab, T* __restrict__ q_rot,
                                                         T* __restrict__ k_rot, T* __restrict__ v_chunk) {
   constexpr int N = Vec<T>::N;                 // elements per 16-byte vector
   const int half = g.d >> 1;
-  const int tpr = half / N;                    // threads per row
-  const long long rows_q = (long long)g.B * g.m * g.Hq;
-  const long long rows_k = (long long)g.B * g.Hkv * (g.S_tot + g.m);
-  const long long rows_v = (long long)g.B * g.m * g.Hkv;
-  const long long total = (rows_q + rows_k + rows_v) * tpr;
-  for (long long task = blockIdx.x * (long long)blockDim.x + threadIdx.x; task < total;
-       task += (long long)gridDim.x * blockDim.x) {
-    long long row = task / tpr;
-    const int t = (int)(task - row * tpr);
+  const int tpr = half / N;                    // threads per row (a power of two)
+  const int tpr_log2 = __ffs(tpr) - 1;
+  const I rows_q = (I)g.B * g.m * g.Hq;
+  const I rows_k = (I)g.B * g.Hkv * (g.S_tot + g.m);
+  const I rows_v = (I)g.B * g.m * g.Hkv;
+  const I total = (rows_q + rows_k + rows_v) * tpr;
+  for (I task = blockIdx.x * (I)blockDim.x + threadIdx.x; task < total; task += (I)gridDim.x * blockDim.x) {
+    I row = task >> tpr_log2;
+    const int t = (int)(task & (tpr - 1));
     const int i0 = t * N;                      // first frequency index of this thread
     if (row < rows_q) {                        // source order (b, r, h): contiguous reads
-      const int h = (int)(row % g.Hq);
-      const long long br = row / g.Hq;
-      const int r = (int)(br % g.m), b = (int)(br / g.m);
-      const uint4* src = reinterpret_cast<const uint4*>(q + row * g.d);
+      const int h = (int)(row % (I)g.Hq);
+      const I br = row / (I)g.Hq;
+      const int r = (int)(br % (I)g.m), b = (int)(br / (I)g.m);
+      const uint4* src = reinterpret_cast<const uint4*>(q + (long long)row * g.d);
       uint4 lo = src[t], hi = src[t + tpr];
       rotate<T>(lo, hi, tab + (long long)(g.n_cached + r) * half + i0);
       uint4* dst = reinterpret_cast<uint4*>(q_rot + (((long long)b * g.Hq + h) * g.ldc + r) * g.d);
@@ -99,9 +101,9 @@ __global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __r
     }
     row -= rows_q;
     if (row < rows_k) {
-      const int ld = g.S_tot + g.m;
+      const I ld = (I)(g.S_tot + g.m);
       const int x = (int)(row % ld);
-      const long long bg = row / ld;
+      const long long bg = (long long)(row / ld);
       const uint4* src;
       int pe;
       if (x < g.S_tot) {
@@ -122,10 +124,10 @@ __global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __r
     }
     row -= rows_k;                             // v_chunk[b][g][r] <- v[b][r][g]
     {
-      const int gg = (int)(row % g.Hkv);
-      const long long br = row / g.Hkv;
-      const int r = (int)(br % g.m), b = (int)(br / g.m);
-      const uint4* src = reinterpret_cast<const uint4*>(v + row * g.d);
+      const int gg = (int)(row % (I)g.Hkv);
+      const I br = row / (I)g.Hkv;
+      const int r = (int)(br % (I)g.m), b = (int)(br / (I)g.m);
+      const uint4* src = reinterpret_cast<const uint4*>(v + (long long)row * g.d);
       uint4* dst = reinterpret_cast<uint4*>(v_chunk + (((long long)b * g.Hkv + gg) * g.ldc + r) * g.d);
       dst[t] = src[t]; dst[t + tpr] = src[t + tpr];
     }
@@ -139,7 +141,10 @@ void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, con
   const long long total = ((long long)g.B * g.Hq * g.m + (long long)g.B * g.Hkv * (g.S_tot + g.m) +
                            (long long)g.B * g.Hkv * g.m) * tpr;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
-  rope_prep_kernel<T><<<blocks, 256, 0, st>>>(g, q, k, v, k_raw_state, rope_tab, q_rot, k_rot, v_chunk);
+  if (total + 148LL * 8 * 256 < (1LL << 31))
+    rope_prep_kernel<T, uint32_t><<<blocks, 256, 0, st>>>(g, q, k, v, k_raw_state, rope_tab, q_rot, k_rot, v_chunk);
+  else
+    rope_prep_kernel<T, long long><<<blocks, 256, 0, st>>>(g, q, k, v, k_raw_state, rope_tab, q_rot, k_rot, v_chunk);
 }
 
 template void launch_rope_prep<float>(const Geometry&, const float*, const float*, const float*,
