@@ -361,3 +361,40 @@ def test_window_span_within_eq4_band_on_gpu(selection):
             o = org[g, 64:]
             span = int(o.max() - o.min() + 1)
             assert S_tilde - slack <= span <= S_tilde, (start, g, span)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_head_sharded_handles_bit_identical(world):
+    """The multi-GPU partition (SURVEY §8(e), configs[4]) through the CUDA path on one device:
+    `world` handles, each owning the kv-head / q-head shard `dist.shard_range` gives a rank,
+    reproduce a single all-heads handle BIT FOR BIT -- outputs of prefill and decode, and the
+    cascade state (origins, mu bit patterns, K/V) of every kv-head (independent heads)."""
+    from paper_2406_17808_b200.dist import shard_range
+    B, Hq, Hkv, d, m = 1, 32, 8, 128, 1024
+    base = dict(batch=B, head_dim=d, sink_size=64, cache_size=4096, num_cascades=4, max_stride=m,
+                dtype="bf16")
+    full = C.Cascade(C.CascadeConfig(num_q_heads=Hq, num_kv_heads=Hkv, **base))
+    shards = [C.Cascade(C.CascadeConfig(num_q_heads=Hq // world, num_kv_heads=Hkv // world, **base))
+              for _ in range(world)]
+    sl = [shard_range(r, world, Hq, Hkv) for r in range(world)]
+    syn = Synth(B, Hq, Hkv, d, seed=5)
+    for start in range(0, 6 * m, m):
+        q, k, v = (t.cuda() for t in syn.chunk(start, m))
+        ref = full.prefill_stride(0, q, k, v)
+        for r, (qs, ks) in enumerate(sl):
+            o = shards[r].prefill_stride(0, q[:, :, qs].contiguous(), k[:, :, ks].contiguous(),
+                                         v[:, :, ks].contiguous())
+            assert torch.equal(o, ref[:, :, qs])
+    for step in range(4):
+        q, k, v = (t[:, 0].contiguous().cuda() for t in syn.chunk(6 * m + step, 1))
+        ref = full.decode(0, q, k, v)
+        for r, (qs, ks) in enumerate(sl):
+            o = shards[r].decode(0, q[:, qs].contiguous(), k[:, ks].contiguous(), v[:, ks].contiguous())
+            assert torch.equal(o, ref[:, qs])
+    torch.cuda.synchronize()
+    st = full.state(0)
+    for r, (qs, ks) in enumerate(sl):
+        sh = shards[r].state(0)
+        assert torch.equal(sh["origin"], st["origin"][:, ks])
+        assert torch.equal(sh["mu"], st["mu"][:, ks])
+        assert torch.equal(sh["k"], st["k"][:, ks]) and torch.equal(sh["v"], st["v"][:, ks])
