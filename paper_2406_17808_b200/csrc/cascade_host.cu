@@ -785,10 +785,13 @@ cascade_status cascade_host_wait(cascade_handle* h) {
 cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,
                               const void* v, void* out, void* stream) {
   // q [B,Hq,d] is [B,1,Hq,d]: the m = 1 case of the strided step (Eq. 2).
-  // the fp32 toy and d = 64 run the m = 1 case of the strided kernels; bf16 d = 128 (the
-  // Llama shapes) has the dedicated HBM-oriented decode kernels
+  // the fp32 toy, d = 64 and GQA groups other than 1 / 2 / 4 / 8 run the m = 1 case of the
+  // strided kernels; bf16 d = 128 with those groups (the Llama shapes) has the dedicated
+  // HBM-oriented decode kernels (instantiated per group size)
   if (h == nullptr || h->cfg.dtype != CASCADE_BF16 || h->cfg.head_dim != 128)
     return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   cascade_status rc = check_call(h, layer, 1);
   if (rc != CASCADE_OK) return rc;
   if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;

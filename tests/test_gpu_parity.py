@@ -176,11 +176,13 @@ def test_cfg2_full_end_to_end_bf16():
     print(f"cfg2: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
 
 
-def test_decode_matches_oracle():
-    """Eq. 2 steps after a short prefill, bf16, GQA 4:1, B = 3."""
-    cfg = C.CascadeConfig(batch=3, num_q_heads=8, num_kv_heads=2, head_dim=128, sink_size=4,
+@pytest.mark.parametrize("Hq", [8, 6])
+def test_decode_matches_oracle(Hq):
+    """Eq. 2 steps after a short prefill, bf16, GQA 4:1 (the dedicated decode kernels) and 3:1
+    (a group size they are not instantiated for: the m = 1 strided path), B = 3."""
+    cfg = C.CascadeConfig(batch=3, num_q_heads=Hq, num_kv_heads=2, head_dim=128, sink_size=4,
                           cache_size=64, num_cascades=4, max_stride=32, dtype="bf16")
-    syn = Synth(3, 8, 2, 128, seed=77)
+    syn = Synth(3, Hq, 2, 128, seed=77)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))
     for start in range(0, 96, 32):
