@@ -81,7 +81,10 @@ typedef struct {
   int32_t num_layers;    /* L >= 1                                              */
   int32_t batch;         /* B >= 1 independent sequences                */
   int32_t num_q_heads;   /* Hq                                                  */
-  int32_t num_kv_heads;  /* Hkv, Hq % Hkv == 0 (GQA)                 */
+  int32_t num_kv_heads;  /* Hkv, Hq % Hkv == 0 (GQA); with BF16 the   */
+                         /* group Hq/Hkv must be <= 8 (the tensor-core score    */
+                         /* pass holds a group's partial sums in shared memory) */
+                         /* else UNSUPPORTED                                    */
   int32_t head_dim;      /* d in {64, 128}                                      */
   int32_t sink_size;     /* alpha >= 0 (64 in the paper)          */
   int32_t cache_size;    /* |C| >= N, excludes the sinks (Q16)           */

@@ -228,6 +228,7 @@ cascade_status cascade_validate_config(const cascade_config* c) {
   if (c->selection != 0 && c->selection != 1) return CASCADE_ERR_CONFIG;
   if (c->head_reduce < 0 || c->head_reduce > 2) return CASCADE_ERR_CONFIG;
   if (c->head_reduce != 0 && c->num_q_heads / c->num_kv_heads > 32) return CASCADE_ERR_UNSUPPORTED;
+  if (c->dtype == CASCADE_BF16 && c->num_q_heads / c->num_kv_heads > 8) return CASCADE_ERR_UNSUPPORTED;
   if (c->head_policy < 0 || c->head_policy > 1) return CASCADE_ERR_CONFIG;
   if (c->head_policy == 1 && c->head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;  // median of all heads
   const long long S = (long long)c->sink_size + c->cache_size;

@@ -54,7 +54,9 @@ def test_ablation_options_validate():
     L = C.lib()
     assert C.validate(C.CascadeConfig(head_reduce="mean", selection=False)) == 0
     assert C.validate(C.CascadeConfig(head_reduce="median")) == 0
-    assert C.validate(C.CascadeConfig(head_reduce="median", num_q_heads=33, num_kv_heads=1)) == -7
+    assert C.validate(C.CascadeConfig(head_reduce="median", num_q_heads=33, num_kv_heads=1, dtype="f32")) == -7
+    assert C.validate(C.CascadeConfig(num_q_heads=32, num_kv_heads=2)) == -7      # bf16 group 16
+    assert C.validate(C.CascadeConfig(num_q_heads=32, num_kv_heads=2, dtype="f32")) == 0
     assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="mean")) == 0
     assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="median")) == -7
     for field, value, code in [("head_reduce", 3, -2), ("selection", 2, -2), ("head_policy", 2, -2)]:
