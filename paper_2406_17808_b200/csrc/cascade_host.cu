@@ -666,11 +666,14 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
       launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
       ps.finish(useful);
     }
-    {
+    if (h->cfg.ema_gamma != 1.0) {
       ProfScope ps(h, 2, st);
       launch_attn_score_tc(tp, L.tm_q, L.tm_k, g.d, st);
       ps.finish(useful);
     }
+    // gamma = 1: every row weight (1 - gamma) gamma^k is 0, so s = 0 exactly (the memset) and
+    // the fold mu <- 1 * mu + 0 leaves mu as it is; pass 2 is skipped (its FMA-pipe exp2 floors
+    // at 2^-126 instead of flushing to 0, which would make the all-zero masses tiny and unequal)
   } else {
     {
       ProfScope ps(h, 1, st);
@@ -683,7 +686,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
       ps.finish(useful);
     }
   }
-  h->launches += 3;
+  h->launches += (std::is_same<T, __nv_bfloat16>::value && h->cfg.ema_gamma == 1.0) ? 2 : 3;
   if (g.homogeneous) {        // one s per sequence, folded by the maintenance launch
     launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
     ++h->launches;

@@ -400,3 +400,32 @@ def test_head_sharded_handles_bit_identical(world):
         assert torch.equal(sh["origin"], st["origin"][:, ks])
         assert torch.equal(sh["mu"], st["mu"][:, ks])
         assert torch.equal(sh["k"], st["k"][:, ks]) and torch.equal(sh["v"], st["v"][:, ks])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("gamma", [1.0, 0.0])
+def test_degenerate_gamma_end_to_end(gamma, dtype):
+    """The EMA's degenerate ends: gamma = 1 gives every row weight 0, so every score is
+    exactly 0, mu never moves and every selection keeps the resident (strict '>', Q2); gamma = 0
+    gives the last row weight 1 and the others 0 (s = that row's P)."""
+    d = 128 if dtype == "bf16" else 64
+    cfg = C.CascadeConfig(batch=1, num_q_heads=8, num_kv_heads=2, head_dim=d, sink_size=4,
+                          cache_size=64, num_cascades=4, max_stride=48, dtype=dtype, ema_gamma=gamma)
+    syn = Synth(1, 8, 2, d, seed=99, dtype=cfg.torch_dtype)
+    gpu = C.Cascade(cfg)
+    orc = CascadeOracle(_oracle_cfg(cfg))
+    start = 0
+    for m in [48, 48, 48, 48, 29]:
+        q, k, v = syn.chunk(start, m)
+        start += m
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        O_ref, s_ref = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL[dtype]
+        sg = _np(gpu.last_scores(0))
+        if gamma == 1.0:
+            assert not sg.any() and not s_ref.any()
+        else:
+            np.testing.assert_allclose(sg, s_ref, rtol=S_RTOL, atol=1e-30)
+        if gamma == 1.0:
+            _compare_state(gpu.state(0), orc.state(0), exact_mu=True)
