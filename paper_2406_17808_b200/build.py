@@ -57,6 +57,7 @@ def _compile(src, force, verbose, extra):
 def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+    extra += os.environ.get("CASCADE_NVCC_EXTRA", "").split()   # e.g. -DCASCADE_PASS1_TRACE
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         results = list(ex.map(lambda s: _compile(s, force, verbose or ptxas_verbose, extra), srcs))

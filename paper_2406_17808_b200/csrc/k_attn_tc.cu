@@ -23,12 +23,26 @@
 #include "tc_util.cuh"
 
 #include <type_traits>
+#include <vector>
+#include <cstdio>
 
 namespace cascade {
 
 namespace {
 constexpr int kTileBytes = 128 * 128;          // one 128-row x 64-col bf16 block (16 KB)
 }
+
+// Optional pass-1 wait accounting (build with CASCADE_NVCC_EXTRA=-DCASCADE_PASS1_TRACE): per
+// CTA, clock64 cycles the MMA issuer spends waiting for K/V tiles and for P, and the softmax
+// warp 4 spends waiting for S, plus the CTA's total; dumped by launch_attn_fwd_tc.
+#ifdef CASCADE_PASS1_TRACE
+__device__ unsigned long long* g_p1_trace = nullptr;
+#define P1_T0() const long long _t0 = clock64()
+#define P1_ACC(v) (v) += clock64() - _t0
+#else
+#define P1_T0()
+#define P1_ACC(v)
+#endif
 
 // Pass 1.  Shared-memory bandwidth (128 B/clk/SM) is the binding resource of a 128x128 MMA
 // with both operands in SMEM, so Q and P live in TMEM (A operand from TMEM, "TS" MMAs) and
@@ -115,9 +129,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 128, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, D, 1);
       const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV);
+#ifdef CASCADE_PASS1_TRACE
+      long long w_kv = 0, w_p = 0;
+      const long long t_start = clock64();
+#endif
       auto qk = [&](int j) {
         const int s = j % kStages;
-        tc::mbar_wait(kv_full + s, (j / kStages) & 1);
+        {
+          P1_T0();
+          tc::mbar_wait(kv_full + s, (j / kStages) & 1);
+          P1_ACC(w_kv);
+        }
         tc::tc_fence_after();
         const uint32_t kbase = aK + s * KB * kTileBytes;
 #pragma unroll
@@ -128,7 +150,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         tc::mma_commit(s_full + (j & 1));
       };
       auto pv = [&](int j) {
-        tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+        {
+          P1_T0();
+          tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+          P1_ACC(w_p);
+        }
         tc::tc_fence_after();
         const uint32_t vbase = aV + (j % kStages) * KB * kTileBytes;
         const uint32_t pbase = tmem + (j & 1) * 128 + 64;
@@ -148,6 +174,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         pv(j);
         if (j + 2 < nt) qk(j + 2);
       }
+#ifdef CASCADE_PASS1_TRACE
+      if (g_p1_trace) {
+        const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        g_p1_trace[cta * 6 + 0] = clock64() - t_start;
+        g_p1_trace[cta * 6 + 1] = w_kv;
+        g_p1_trace[cta * 6 + 2] = w_p;
+        g_p1_trace[cta * 6 + 5] = nt;
+      }
+#endif
     }
   } else if (warp >= 4) {
     // ---------------- softmax warpgroup ----------------
@@ -174,9 +209,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     }
     float m_used = -INFINITY, l = 0.f;
     float x[128];
+#ifdef CASCADE_PASS1_TRACE
+    long long w_s = 0, w_pv = 0;
+#endif
     for (int j = 0; j < nt; ++j) {
       const uint32_t sb = tmem + (j & 1) * 128 + lane_off;
-      tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+      {
+        P1_T0();
+        tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+        P1_ACC(w_s);
+      }
       tc::tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) tc::tmem_ld32(sb + c * 32, x + c * 32);
@@ -242,7 +284,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         const float mx = mraw * p.scale_log2;
         const bool need = mx > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
-          tc::mbar_wait(pv_done, (j - 1) & 1);
+          {
+            P1_T0();
+            tc::mbar_wait(pv_done, (j - 1) & 1);
+            P1_ACC(w_pv);
+          }
           tc::tc_fence_after();
           const float f = need ? tc::fast_exp2(m_used - mx) : 1.f;
 #pragma unroll
@@ -271,6 +317,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     // satisfied by phase nt-3: wait for nt-2 first, then nt-1.
     if (nt >= 2) tc::mbar_wait(pv_done, (nt - 2) & 1);
     tc::mbar_wait(pv_done, (nt - 1) & 1);
+#ifdef CASCADE_PASS1_TRACE
+    if (g_p1_trace && threadIdx.x == 128) {
+      const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      g_p1_trace[cta * 6 + 3] = w_s;
+      g_p1_trace[cta * 6 + 4] = w_pv;
+    }
+#endif
     tc::tc_fence_after();
     const float inv = 1.f / l;
     const bool store = qi < p.m;
@@ -546,8 +599,29 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 256, smem, st>>>(tq, tk, tvs, tvc, p);
   };
+#ifdef CASCADE_PASS1_TRACE
+  static unsigned long long* trace = nullptr;
+  static int calls = 0;
+  const long long ctas = (long long)grid.x * grid.y * grid.z;
+  if (!trace) {
+    cudaMalloc(&trace, 8 * 6 * 4096LL * 64);
+    cudaMemcpyToSymbol(g_p1_trace, &trace, sizeof(trace));
+  }
+#endif
   if (d == 128) go(attn_fwd_tc_kernel<128, 4>);
   else go(attn_fwd_tc_kernel<64, 4>);
+#ifdef CASCADE_PASS1_TRACE
+  if (++calls % 16 == 0 && ctas <= 4096LL * 64) {
+    std::vector<unsigned long long> h(ctas * 6);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (long long c = 0; c < ctas; ++c)
+      for (int k = 0; k < 6; ++k) a[k] += (double)h[c * 6 + k];
+    std::fprintf(stderr, "pass1 trace (call %d, %lld CTAs, %.1f tiles/CTA): per tile: CTA %.0f clk | MMA waits K/V %.0f, P %.0f | softmax waits S %.0f, PV(rescale) %.0f\n",
+                 calls, ctas, a[5] / ctas, a[0] / a[5], a[1] / a[5], a[2] / a[5], a[3] / a[5], a[4] / a[5]);
+  }
+#endif
 }
 
 void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk, int d,
