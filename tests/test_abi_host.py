@@ -124,3 +124,14 @@ def test_cfg3_schedule_is_depth_zero_and_fill_trajectory():
         assert ops[3] <= 1
     assert mirror.t == 1 << 20
     assert sum(mirror.counts[:8]) < 65536
+
+
+def test_binding_fails_loudly_without_the_library(monkeypatch, tmp_path):
+    """No CPU fallback: with the shared library absent the binding raises instead of computing
+    anything elsewhere (the product path must fail loudly)."""
+    monkeypatch.setattr(C, "_lib", None)
+    monkeypatch.setattr(C, "LIB_PATH", str(tmp_path / "libcascade.so"))
+    with pytest.raises(RuntimeError, match="missing"):
+        C.lib()
+    with pytest.raises(RuntimeError, match="missing"):
+        C.validate(C.CascadeConfig())
