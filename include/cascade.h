@@ -48,9 +48,16 @@
  * A handle is single-writer: do not call into one handle from two threads.
  *
  * Errors: every entry point validates on the host before launching anything;
- * on a non-OK return no device state changed and the mirror did not advance.
- * CASCADE_ERR_CUDA reports a launch/copy error (cudaGetLastError); device
- * faults surface at the next synchronisation, as CUDA does.
+ * a validation error (INVALID_ARG, CONFIG, SHAPE, ORDER, WORKSPACE,
+ * UNSUPPORTED) leaves the device state and the host mirror untouched.  Each
+ * call first clears any stale (non-sticky) CUDA error left by earlier runtime
+ * calls, then checks every launch and copy it issues.  CASCADE_ERR_CUDA
+ * returned before the first state-mutating kernel (the EMA fold in pass 2 or
+ * the score-injection fold, maintenance, the decode update) means nothing
+ * changed; once such a kernel is enqueued a CUDA error POISONS the handle:
+ * the call returns CASCADE_ERR_CUDA and every later call on the handle returns
+ * CASCADE_ERR_POISONED (device state and mirror may disagree; destroy the
+ * handle).  Device faults surface at the next synchronisation, as CUDA does.
  */
 #ifndef CASCADE_H_
 #define CASCADE_H_
@@ -72,7 +79,9 @@ typedef enum {
   CASCADE_ERR_ORDER = -4,       /* reserved: call out of order                   */
   CASCADE_ERR_WORKSPACE = -5,   /* workspace too small or misaligned             */
   CASCADE_ERR_CUDA = -6,        /* CUDA launch / copy error                      */
-  CASCADE_ERR_UNSUPPORTED = -7  /* option not implemented in this build         */
+  CASCADE_ERR_UNSUPPORTED = -7, /* option not implemented in this build         */
+  CASCADE_ERR_POISONED = -8     /* an earlier call failed after state-mutating   */
+                                /* kernels were enqueued: destroy the handle     */
 } cascade_status;
 
 typedef enum { CASCADE_F32 = 0, CASCADE_BF16 = 1 } cascade_dtype;

@@ -20,7 +20,8 @@ LIB_PATH = os.path.join(HERE, "libcascade.so")
 MAX_LEVELS = 16
 F32, BF16 = 0, 1
 _STATUS = {0: "ok", -1: "invalid argument", -2: "invalid config", -3: "bad shape",
-           -4: "call out of order", -5: "workspace", -6: "CUDA error", -7: "unsupported"}
+           -4: "call out of order", -5: "workspace", -6: "CUDA error", -7: "unsupported",
+           -8: "handle poisoned by an earlier CUDA error"}
 
 
 class CascadeError(RuntimeError):
@@ -188,7 +189,28 @@ def mirror_advance(cfg: CascadeConfig, mirror: Mirror, m: int, want_pe=True, wan
 
 
 class Cascade:
-    """One library handle: the cascades of every (layer, sequence, kv-head) on one device."""
+    """One library handle: the cascades of every (layer, sequence, kv-head) on one device.
+
+    The C ABI receives raw pointers and cannot check shapes, so every call checks here that
+    each tensor has the shape, dtype, layout and device the handle's config implies (a wrong
+    tensor would otherwise read or write out of bounds)."""
+
+    def _check_io(self, ts, shapes, on_device=True, names=("q", "k", "v", "out")):
+        for name, t, shape in zip(names, ts, shapes):
+            if tuple(t.shape) != tuple(shape):
+                raise ValueError(f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
+            if t.dtype != self.cfg.torch_dtype or not t.is_contiguous():
+                raise ValueError(f"{name}: needs a contiguous {self.cfg.torch_dtype} tensor")
+            if on_device and t.device != self.device:
+                raise ValueError(f"{name}: on {t.device}, the handle is on {self.device}")
+            if not on_device and t.is_cuda:
+                raise ValueError(f"{name}: the host-buffer call takes host tensors")
+
+    def _chunk_shapes(self, m):
+        c = self.cfg
+        qs = (c.batch, m, c.num_q_heads, c.head_dim)
+        ks = (c.batch, m, c.num_kv_heads, c.head_dim)
+        return qs, ks, ks, qs
 
     def __init__(self, cfg: CascadeConfig, device: int = 0):
         self.cfg = cfg
@@ -220,11 +242,10 @@ class Cascade:
     # ---- hot path ------------------------------------------------------------
     def prefill_stride(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                        out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-        B, m, Hq, d = q.shape
+        m = q.shape[1]
         if out is None:
             out = torch.empty_like(q)
-        for t in (q, k, v, out):
-            assert t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        self._check_io((q, k, v, out), self._chunk_shapes(m))
         rc = lib().cascade_prefill_stride(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m, _ptr(out),
                                           _stream(stream))
         _check(rc, "cascade_prefill_stride")
@@ -234,8 +255,7 @@ class Cascade:
                             out: torch.Tensor, stream=None) -> torch.Tensor:
         """q/k/v/out are (pinned) host tensors; copies happen inside the library call."""
         m = q.shape[1]
-        for t in (q, k, v, out):
-            assert not t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        self._check_io((q, k, v, out), self._chunk_shapes(m), on_device=False)
         rc = lib().cascade_prefill_stride_host(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m,
                                                _ptr(out), _stream(stream))
         _check(rc, "cascade_prefill_stride_host")
@@ -245,8 +265,7 @@ class Cascade:
                                   out: torch.Tensor, stream=None) -> torch.Tensor:
         """Pipelined host-buffer step: returns at once; `out` is valid after host_wait()."""
         m = q.shape[1]
-        for t in (q, k, v, out):
-            assert not t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        self._check_io((q, k, v, out), self._chunk_shapes(m), on_device=False)
         rc = lib().cascade_prefill_stride_host_async(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m,
                                                      _ptr(out), _stream(stream))
         _check(rc, "cascade_prefill_stride_host_async")
@@ -259,8 +278,9 @@ class Cascade:
                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         if out is None:
             out = torch.empty_like(q)
-        for t in (q, k, v, out):
-            assert t.is_cuda and t.is_contiguous() and t.dtype == self.cfg.torch_dtype
+        c = self.cfg
+        qs, ks = (c.batch, c.num_q_heads, c.head_dim), (c.batch, c.num_kv_heads, c.head_dim)
+        self._check_io((q, k, v, out), (qs, ks, ks, qs))
         rc = lib().cascade_decode(self._h, layer, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _stream(stream))
         _check(rc, "cascade_decode")
         return out
@@ -269,8 +289,12 @@ class Cascade:
     def update_with_scores(self, layer: int, k: torch.Tensor, v: torch.Tensor, s: torch.Tensor,
                            stream=None) -> None:
         m = k.shape[1]
-        assert s.dtype == torch.float32 and s.is_cuda and s.is_contiguous()
-        assert s.shape == (self.cfg.batch, self.cfg.num_kv_heads, self.cfg.s_tot + m)
+        _, ks, _, _ = self._chunk_shapes(m)
+        self._check_io((k, v), (ks, ks), names=("k", "v"))
+        if s.dtype != torch.float32 or s.device != self.device or not s.is_contiguous():
+            raise ValueError("s: needs a contiguous float32 tensor on the handle's device")
+        if tuple(s.shape) != (self.cfg.batch, self.cfg.num_kv_heads, self.cfg.s_tot + m):
+            raise ValueError(f"s: shape {tuple(s.shape)}")
         rc = lib().cascade_update_with_scores(self._h, layer, _ptr(k), _ptr(v), m, _ptr(s),
                                               _stream(stream))
         _check(rc, "cascade_update_with_scores")

@@ -158,6 +158,9 @@ struct cascade_handle {
   cudaEvent_t ring_ev[kRing];
   int ring_pos;
   int64_t launches;
+  // set when a CUDA error is detected after a state-mutating kernel was enqueued: the device
+  // state and the host mirror may disagree, so every later call is refused (cascade.h, Errors)
+  bool poisoned;
   // profiling (cascade_profile_*)
   bool profiling;
   struct Rec { cudaEvent_t a, b; double work; };
@@ -208,6 +211,7 @@ const char* cascade_status_string(cascade_status s) {
     case CASCADE_ERR_WORKSPACE: return "workspace too small or misaligned";
     case CASCADE_ERR_CUDA: return "CUDA error";
     case CASCADE_ERR_UNSUPPORTED: return "unsupported option";
+    case CASCADE_ERR_POISONED: return "handle poisoned by an earlier CUDA error (destroy it)";
   }
   return "unknown status";
 }
@@ -302,6 +306,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->S_tot = h->alpha + cfg->cache_size;
   h->planner.configure(h->alpha, h->N, h->c, h->cfg.selection != 0);
   h->launches = 0;
+  h->poisoned = false;
   h->ring_pos = 0;
   h->profiling = false;
   h->moved_seen = 0;
@@ -459,47 +464,18 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   *next = pre;
   h->planner.advance(*next, m, &h->plan);
   const Plan& P = h->plan;
-  const int slot = h->ring_pos;
-  h->ring_pos = (h->ring_pos + 1) % kRing;
-  if (cudaEventSynchronize(h->ring_ev[slot]) != cudaSuccess) return CASCADE_ERR_CUDA;
-  int32_t* buf = h->pinned[slot];
   const size_t nsel = P.sel.size(), nord = P.sel_order.size(), nmov = P.mov.size();
-  std::memcpy(buf, P.sel.data(), nsel * 4);
-  std::memcpy(buf + nsel, P.sel_order.data(), nord * 4);
-  std::memcpy(buf + nsel + nord, P.mov.data(), nmov * 4);
-  float* w = reinterpret_cast<float*>(buf + nsel + nord + nmov);
-  float* lw = w + m;
-  const double gam = h->cfg.ema_gamma;
-  for (int32_t r = 0; r < m; ++r) {    // C_EMA = (1 - gamma) gamma^(m-1-r)  (Alg. 3, P:644)
-    const double wr = (1.0 - gam) * gamma_pow(gam, m - 1 - r);
-    w[r] = (float)wr;
-    lw[r] = wr > 0 ? (float)std::log2(wr) : -INFINITY;
-  }
   // resident key tiles: valid runs (sinks, then sub-caches 1..N) cut into 128-slot tiles
-  auto pad4 = [](size_t x) { return (x + 3) & ~size_t(3); };       // int2 / int4 alignment
-  const size_t tiles_off = pad4(nsel + nord + nmov + 2 * (size_t)m);
-  int32_t* tiles = buf + tiles_off;
-  int32_t nt = 0;
+  std::vector<int2> tiles;
   auto add_run = [&](int32_t beg, int32_t len) {
-    for (int32_t o = 0; o < len; o += 128) {
-      tiles[2 * nt] = beg + o;
-      tiles[2 * nt + 1] = std::min(128, len - o);
-      ++nt;
-    }
+    for (int32_t o = 0; o < len; o += 128) tiles.push_back(make_int2(beg + o, std::min(128, len - o)));
   };
   add_run(0, pre.sink_count);
   for (int32_t i = 0; i < h->N; ++i) add_run(h->alpha + i * h->c, pre.counts[i]);
-  int32_t* phases = tiles + 2 * nt;                  // (2 nt ints: phases stay 4-aligned + 2 nt)
-  for (size_t i = 0; i < P.phase_begin.size(); ++i) phases[i] = P.phase_begin[i];
   // the same runs as 128-slot tiles with their rank geometry for decode: pe of key j = pe0 + j;
   // a tile of a full ring is split where the ring wraps past its oldest slot xi
-  const size_t dt_off = pad4(tiles_off + 2 * (size_t)nt + P.phase_begin.size());
-  int32_t* dt = buf + dt_off;
-  int32_t ndt = 0;
-  auto add_dec = [&](int32_t x0, int32_t len, int32_t pe0, int32_t jw) {
-    dt[4 * ndt] = x0; dt[4 * ndt + 1] = len; dt[4 * ndt + 2] = pe0; dt[4 * ndt + 3] = jw; ++ndt;
-  };
-  for (int32_t o = 0; o < pre.sink_count; o += 128) add_dec(o, std::min(128, pre.sink_count - o), o, 128);
+  std::vector<int4> dt;
+  for (int32_t o = 0; o < pre.sink_count; o += 128) dt.push_back(make_int4(o, std::min(128, pre.sink_count - o), o, 128));
   {
     int32_t base = pre.sink_count;
     int32_t bases[CASCADE_MAX_LEVELS];
@@ -510,17 +486,16 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
       for (int32_t s0 = 0; s0 < cnt; s0 += 128) {
         const int32_t len = std::min(128, cnt - s0);
         const int32_t x0 = h->alpha + i * c + s0;
-        if (!full) { add_dec(x0, len, bases[i] + s0, 128); continue; }
-        if (s0 >= xi) { add_dec(x0, len, bases[i] + s0 - xi, 128); continue; }
+        if (!full) { dt.push_back(make_int4(x0, len, bases[i] + s0, 128)); continue; }
+        if (s0 >= xi) { dt.push_back(make_int4(x0, len, bases[i] + s0 - xi, 128)); continue; }
         const int32_t before = std::min(len, xi - s0);         // slots s0 .. xi-1: newest part
-        add_dec(x0, before, bases[i] + s0 - xi + c, 128);
-        if (before < len) add_dec(x0 + before, len - before, bases[i], 128);
+        dt.push_back(make_int4(x0, before, bases[i] + s0 - xi + c, 128));
+        if (before < len) dt.push_back(make_int4(x0 + before, len - before, bases[i], 128));
       }
     }
   }
   // maintenance moves, in phase order (C_N .. C_1, sinks): those that read a resident slot
   // (evictees, selections) and those that read only chunk rows
-  const size_t mi_off = pad4(dt_off + 4 * (size_t)ndt);
   const int32_t S_tot = h->S_tot;
   std::vector<int32_t>& rd = h->maint_reads;
   auto reads = [&](int32_t ref, auto&& self) -> void {    // concrete slots a reference reads
@@ -541,11 +516,38 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
     reads(ref, reads);
     (rd.empty() ? chunk_moves : staged).push_back(make_int4(dst, ref, cand, inc));
   }
-  std::memcpy(buf + mi_off, staged.data(), staged.size() * sizeof(int4));
+  // layout of the upload (int32 words): sel | sel_order | mov | w [m] | log2w [m] | tiles (int2) |
+  // phase_begin | dec tiles (int4) | staged moves (int4) | chunk moves (int4); every capacity is
+  // checked before anything is written into the pinned buffer
+  auto pad4 = [](size_t x) { return (x + 3) & ~size_t(3); };       // int2 / int4 alignment
+  const size_t w_off = nsel + nord + nmov;
+  const size_t tiles_off = pad4(w_off + 2 * (size_t)m);
+  const size_t ph_off = tiles_off + 2 * tiles.size();
+  const size_t dt_off = pad4(ph_off + P.phase_begin.size());
+  const size_t mi_off = pad4(dt_off + 4 * dt.size());
   const size_t cm_off = mi_off + 4 * staged.size();
-  std::memcpy(buf + cm_off, chunk_moves.data(), chunk_moves.size() * sizeof(int4));
   const size_t total = cm_off + 4 * chunk_moves.size();
   if (total > (size_t)h->sz.plan_ints) return CASCADE_ERR_WORKSPACE;   // capacity formula broken
+  const int slot = h->ring_pos;
+  if (cudaEventSynchronize(h->ring_ev[slot]) != cudaSuccess) return CASCADE_ERR_CUDA;
+  h->ring_pos = (h->ring_pos + 1) % kRing;
+  int32_t* buf = h->pinned[slot];
+  std::memcpy(buf, P.sel.data(), nsel * 4);
+  std::memcpy(buf + nsel, P.sel_order.data(), nord * 4);
+  std::memcpy(buf + nsel + nord, P.mov.data(), nmov * 4);
+  float* w = reinterpret_cast<float*>(buf + w_off);
+  float* lw = w + m;
+  const double gam = h->cfg.ema_gamma;
+  for (int32_t r = 0; r < m; ++r) {    // C_EMA = (1 - gamma) gamma^(m-1-r)  (Alg. 3, P:644)
+    const double wr = (1.0 - gam) * gamma_pow(gam, m - 1 - r);
+    w[r] = (float)wr;
+    lw[r] = wr > 0 ? (float)std::log2(wr) : -INFINITY;
+  }
+  std::memcpy(buf + tiles_off, tiles.data(), tiles.size() * sizeof(int2));
+  std::memcpy(buf + ph_off, P.phase_begin.data(), P.phase_begin.size() * 4);
+  std::memcpy(buf + dt_off, dt.data(), dt.size() * sizeof(int4));
+  std::memcpy(buf + mi_off, staged.data(), staged.size() * sizeof(int4));
+  std::memcpy(buf + cm_off, chunk_moves.data(), chunk_moves.size() * sizeof(int4));
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -555,13 +557,13 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   pd->mov = L.plan + nsel + nord;
   pd->resolved = L.resolved;
   pd->sel_cap = h->cfg.max_stride;
-  up->w = reinterpret_cast<const float*>(L.plan + nsel + nord + nmov);
+  up->w = reinterpret_cast<const float*>(L.plan + w_off);
   up->log2w = up->w + m;
   up->tiles = reinterpret_cast<const int2*>(L.plan + tiles_off);
-  up->n_tiles = nt;
-  up->phase_begin = L.plan + tiles_off + 2 * nt;
+  up->n_tiles = (int32_t)tiles.size();
+  up->phase_begin = L.plan + ph_off;
   up->dec_tiles = reinterpret_cast<const int4*>(L.plan + dt_off);
-  up->n_dec_tiles = ndt;
+  up->n_dec_tiles = (int32_t)dt.size();
   up->maint_staged = reinterpret_cast<const int4*>(L.plan + mi_off);
   up->n_maint_staged = (int32_t)staged.size();
   up->maint_chunk = reinterpret_cast<const int4*>(L.plan + cm_off);
@@ -587,8 +589,21 @@ uint64_t moved_total(cascade_handle* h) {
   return tot;
 }
 
+// CUDA status of the launches issued since the last check (and clears it).
+inline bool launches_ok() { return cudaGetLastError() == cudaSuccess; }
+
+// A CUDA error after a state-mutating kernel was enqueued: the device state may have moved
+// while the mirror did not, so the handle refuses every later call (cascade.h, Errors).
+cascade_status poison(cascade_handle* h) {
+  h->poisoned = true;
+  return CASCADE_ERR_CUDA;
+}
+
+// Maintenance of one chunk: the EMA fold when the score producer did not fold, deep selections,
+// then the cooperative move launch.  Every launch here mutates state; returns false on a launch
+// error (the caller poisons the handle).
 template <typename T>
-void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up,
+bool launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up,
                         const T* k, const T* v, const float* s, bool folded, cudaStream_t st) {
   const Plan& P = h->plan;
   const PlanDev& pd = up.pd;
@@ -606,6 +621,7 @@ void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
       ++h->launches;
     }
   }
+  if (!launches_ok()) return false;
   MaintItems it{};
   it.inline_sel = deep ? 0 : 1;
   it.moved = maint_moved_ptr(h, L);
@@ -615,9 +631,11 @@ void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
   it.n_chunk = up.n_maint_chunk;
   it.barrier = L.maint_ctl;
   it.barrier_base = L.maint_barrier;
-  L.maint_barrier += (uint32_t)maint_barriers<T>(g, it);
   StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin, k, v};
-  launch_maint<T>(g, pd, it, sd, s, st);
+  // the host copy of the grid-barrier counter advances only when the launch was accepted, so a
+  // refused launch cannot leave the next one spinning on arrivals that never happen
+  if (launch_maint<T>(g, pd, it, sd, s, st) != cudaSuccess) return false;
+  L.maint_barrier += (uint32_t)maint_barriers<T>(g, it);
   h->launches += (up.n_maint_staged > 0 || up.n_maint_chunk > 0) ? 1 : 0;
   h->moved_chunk += (uint64_t)up.n_maint_chunk * g.B * g.Hkv;
   // algorithmic bytes: EMA 20 B per resident (mu r/w + s) when folded here; each row actually
@@ -625,6 +643,7 @@ void launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
   // added by cascade_profile_read
   const double bg = (double)g.B * g.Hkv;
   ps.finish(folded ? 0.0 : bg * 20.0 * g.n_cached);
+  return true;
 }
 
 template <typename T>
@@ -636,22 +655,23 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
   cascade_mirror next;
   cascade_status rc = upload_plan(h, layer, m, st, &up, &next);
   if (rc != CASCADE_OK) return rc;
-  const PlanDev& pd = up.pd;
   T* q_rot = reinterpret_cast<T*>(L.q_rot);
   T* k_rot = reinterpret_cast<T*>(L.k_rot);
   T* v_chunk = reinterpret_cast<T*>(L.v_chunk);
   const double es = sizeof(T);
   const double pairs = (double)g.B * g.Hq * ((double)m * g.n_cached + 0.5 * (double)m * (m + 1));
   const double useful = 4.0 * g.d * pairs;
+  constexpr bool kTc = std::is_same<T, __nv_bfloat16>::value;
   {
     ProfScope ps(h, 0, st);
     launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, q_rot, k_rot,
                         v_chunk, st);
     ps.finish(2.0 * es * g.d * ((double)g.B * g.Hq * m + (double)g.B * g.Hkv * (g.n_cached + 2.0 * m)));
   }
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+  // scratch only so far (rotated operands); pass 1 writes `out` and the row LSEs
+  TcParams tp{};
+  if constexpr (kTc) {
     // tcgen05 path: pass 1 (O, LSE) then the key-stationary exact-mass pass 2
-    TcParams tp{};
     tp.B = g.B; tp.Hq = g.Hq; tp.Hkv = g.Hkv; tp.G = g.G; tp.m = m; tp.M = g.ldc; tp.S_tot = g.S_tot;
     tp.Mb = (g.ldc + 127) / 128 * 128;
     tp.scale_log2 = g.scale_log2;
@@ -660,40 +680,42 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     tp.mu = g.homogeneous ? nullptr : L.mu;   // pass 2 folds the EMA in its epilogue
     tp.decay = g.decay;
     tp.head_reduce = g.head_reduce;
-    cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st);
-    {
-      ProfScope ps(h, 1, st);
-      launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
-      ps.finish(useful);
-    }
+    if (cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st) != cudaSuccess)
+      return CASCADE_ERR_CUDA;
+    ProfScope ps(h, 1, st);
+    launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
+    ps.finish(useful);
+  } else {
+    ProfScope ps(h, 1, st);
+    launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
+    ps.finish(useful);
+  }
+  h->launches += 2;
+  if (!launches_ok()) return CASCADE_ERR_CUDA;   // nothing of the cascade state has changed yet
+  // from here on every launch mutates the cascade state (pass 2 folds mu in its epilogue)
+  if constexpr (kTc) {
     if (h->cfg.ema_gamma != 1.0) {
       ProfScope ps(h, 2, st);
       launch_attn_score_tc(tp, L.tm_q, L.tm_k, g.d, st);
       ps.finish(useful);
+      ++h->launches;
     }
     // gamma = 1: every row weight (1 - gamma) gamma^k is 0, so s = 0 exactly (the memset) and
     // the fold mu <- 1 * mu + 0 leaves mu as it is; pass 2 is skipped (its FMA-pipe exp2 floors
     // at 2^-126 instead of flushing to 0, which would make the all-zero masses tiny and unequal)
   } else {
-    {
-      ProfScope ps(h, 1, st);
-      launch_attn_fwd_simt<T>(g, q_rot, k_rot, reinterpret_cast<const T*>(L.v), v_chunk, out, L.lse, st);
-      ps.finish(useful);
-    }
-    {
-      ProfScope ps(h, 2, st);
-      launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, up.w, L.s, st);
-      ps.finish(useful);
-    }
+    ProfScope ps(h, 2, st);
+    launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, up.w, L.s, st);
+    ps.finish(useful);
+    ++h->launches;
   }
-  h->launches += (std::is_same<T, __nv_bfloat16>::value && h->cfg.ema_gamma == 1.0) ? 2 : 3;
   if (g.homogeneous) {        // one s per sequence, folded by the maintenance launch
     launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
     ++h->launches;
   }
-  launch_maintenance<T>(h, g, L, up, k, v, L.s,
-                        /*folded=*/std::is_same<T, __nv_bfloat16>::value && !g.homogeneous, st);
-  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  if (!launches_ok()) return poison(h);
+  if (!launch_maintenance<T>(h, g, L, up, k, v, L.s, /*folded=*/kTc && !g.homogeneous, st) || !launches_ok())
+    return poison(h);
   h->mirrors[layer] = next;   // commit the mirror
   h->m_last[layer] = m;
   return CASCADE_OK;
@@ -701,6 +723,8 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
 
 cascade_status check_call(cascade_handle* h, int32_t layer, int32_t m) {
   if (!h) return CASCADE_ERR_INVALID_ARG;
+  if (h->poisoned) return CASCADE_ERR_POISONED;
+  (void)cudaGetLastError();   // a stale non-sticky error of an earlier runtime call is not ours
   if (layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
   if (m < 1 || m > h->cfg.max_stride) return CASCADE_ERR_SHAPE;
   return CASCADE_OK;
@@ -735,6 +759,8 @@ cascade_status cascade_prefill_stride_host(cascade_handle* h, int32_t layer, con
   const size_t es = elem_size(h->cfg.dtype);
   const size_t nq = (size_t)h->cfg.batch * m * h->cfg.num_q_heads * h->cfg.head_dim * es;
   const size_t nk = (size_t)h->cfg.batch * m * h->cfg.num_kv_heads * h->cfg.head_dim * es;
+  // staging set 0 may still be in use by a pipelined call (its output copy is the last use)
+  if (h->stage_used[0] && cudaStreamWaitEvent(st, h->ev_out[0], 0) != cudaSuccess) return CASCADE_ERR_CUDA;
   if (cudaMemcpyAsync(h->stage_q, q, nq, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(h->stage_k, k, nk, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(h->stage_v, v, nk, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -838,7 +864,7 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
     ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 4.0 * g.G + 16.0 + 4.0));
   }
   h->launches += g.homogeneous ? 5 : 3;
-  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  if (!launches_ok()) return poison(h);   // the update kernel folds mu and moves rows
   h->mirrors[layer] = next;
   h->m_last[layer] = 1;
   return CASCADE_OK;
@@ -859,18 +885,19 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   const PlanDev& pd = up.pd;
   if (g.homogeneous) {        // the injected kv-head scores reduced per sequence
     const size_t n = (size_t)g.B * g.Hkv * (g.S_tot + m);
-    cudaMemcpyAsync(L.s, s, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    if (cudaMemcpyAsync(L.s, s, n * sizeof(float), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return CASCADE_ERR_CUDA;
     launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
     ++h->launches;
+    if (!launches_ok()) return CASCADE_ERR_CUDA;   // scratch only so far
     s = L.s;
   }
-  if (h->cfg.dtype == CASCADE_BF16)
-    launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
-                                      static_cast<const __nv_bfloat16*>(v), s, false, st);
-  else
-    launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k), static_cast<const float*>(v), s, false,
-                              st);
-  if (cudaGetLastError() != cudaSuccess) return CASCADE_ERR_CUDA;
+  const bool ok = h->cfg.dtype == CASCADE_BF16
+                      ? launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
+                                                          static_cast<const __nv_bfloat16*>(v), s, false, st)
+                      : launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k),
+                                                  static_cast<const float*>(v), s, false, st);
+  if (!ok || !launches_ok()) return poison(h);
   h->mirrors[layer] = next;
   h->m_last[layer] = 0;
   return CASCADE_OK;
@@ -891,6 +918,7 @@ cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out,
 
 cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   if (!h || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (h->poisoned) return CASCADE_ERR_POISONED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
@@ -936,6 +964,8 @@ cascade_status cascade_profile_read(cascade_handle* h, double* ms, int64_t* coun
 
 cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out, void* stream) {
   if (!h || !out || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (h->poisoned) return CASCADE_ERR_POISONED;
+  (void)cudaGetLastError();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   const cascade_mirror& mr = h->mirrors[layer];

@@ -100,7 +100,7 @@ struct MaintItems {
 };
 struct MaintGrid { int blocks, rows_per_block; };
 template <typename T>
-void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
+cudaError_t launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
                   cudaStream_t st);
 // barrier arrivals one launch adds (the host advances barrier_base by it)
 template <typename T>

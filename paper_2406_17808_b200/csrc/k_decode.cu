@@ -1,15 +1,12 @@
 // k_decode.cu -- single-token step (Eq. 2) + its cascade update, bf16.
 //
-// Decode is HBM-bound (every cached K/V row is read once per step, 4 flop/byte), so it runs
-// on the SIMT pipes -- no tensor-core reshaping:
-//   decode_attn     grid (split, b*Hkv): each CTA streams a contiguous range of the valid keys
-//                   (sinks, C_1..C_N in slot order, then the new token) through a 2-stage
-//                   cp.async ring of 64-key tiles.  Two threads per key rotate the pre-RoPE key
-//                   to its cache rank pe (cos/sin of pe*theta_i by angle addition from
-//                   two small fp64-built tables), round it to bf16 (reading Q17: the operand
-//                   the paper's bf16 model consumes), dot it with the G rotated queries of the
-//                   group and write the log2-domain logits; an online softmax accumulates
-//                   O = P V per (head, dim) and the split's (max, sum).
+// Decode is HBM-bound (every cached K/V row is read once per step, ~4 flop/byte); the dot
+// products still run on the tensor cores (tcgen05, M = 128 keys x N = 16 query columns) so the
+// SIMT pipes are free for the per-key rotation and softmax:
+//   decode_attn     grid (b*Hkv, split): TMA-fed, warp-specialised (below); each CTA streams a
+//                   contiguous range of 128-slot key tiles, rotates every raw key in shared
+//                   memory to its rank pe, S^T = K_rot Q^T and O^T += V^T P^T in TMEM,
+//                   writes the log2-domain logits and the split's (max, sum, O).
 //   decode_combine  one CTA per (b, q-head): merges the splits -> O (bf16) and lse2.
 //   decode_update   one CTA per (b, g): exact mass s = w_0 * max_h exp2(logit_h - lse2_h)
 //                   (Alg. 3 with m = 1: w_0 = 1 - gamma; max over the group), EMA fold

@@ -12,17 +12,18 @@
 //     i.e. m > c wraps a level): winner = cand if mu(cand) > mu(inc) else inc (strict '>',
 //     P:615), per (b, g), one launch per dependency depth.  Depth-0 selections -- all of them
 //     in every benchmark config -- are resolved inside the block that moves the winner.
-//  2. maint: ONE launch, a block per (item, b*g).  An item is a run of <= 64 moves of one
-//     phase (phases C_N, ..., C_1, sinks; destinations sorted), with at most kMaintStaged
-//     moves that read a resident slot.  Hazard: a move's source may be a pre-chunk slot that
-//     another item overwrites (an evictee carried to the next sub-cache).  The host
-//     lists, per item, the items that READ its destinations (always earlier items, deeper
-//     sub-caches); a block loads resident sources into shared memory (cp.async), publishes
-//     "loaded" (a per-(item, b*g) epoch flag), waits only for the flags of its readers, then
-//     stores.  Chunk-row sources are never overwritten: copied after the wait, straight
-//     through registers.
+//  2. maint_coop_kernel: ONE cooperative launch per chunk for all (b, g).  The host splits the
+//     chunk's final moves {dst, ref, cand, inc} into "staged" moves that read a pre-chunk
+//     resident slot (evictees carried to the next sub-cache, and selections,
+//     P:611-619) and "chunk" moves that read only chunk rows.  The hazard is a staged move's
+//     source being overwritten by another move of the same chunk, so staged rows are loaded
+//     GPU-wide into shared memory (TMA bulk copies, selections resolved in place), all blocks
+//     meet at one relaxed grid barrier, then the rows are bulk-stored; chunk moves (never
+//     overwritten sources) fill the spare shared-memory rows and stream after the barrier.
+//     A chunk whose staged moves exceed one round's shared memory runs several rounds, each
+//     with its own barrier, in phase order (readers of a slot always precede its writer).
 //
-// All HBM-bound: coalesced 16-byte vectors, a full warp per moved (K | V) row pair.
+// All HBM-bound: 256-B rows moved by TMA bulk copies, mu / origin by the row's thread.
 #include "common.cuh"
 #include "tc_util.cuh"
 
@@ -185,9 +186,16 @@ __global__ void __launch_bounds__(kCoopThreads, 2) maint_coop_kernel(Geometry g,
       if (fenced) __threadfence();
       asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(it.barrier) : "memory");
       uint32_t v;
-      while (true) {
+      unsigned long long t_begin;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+      for (uint32_t spin = 0;; ++spin) {
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(it.barrier) : "memory");
         if ((int32_t)(v - bar) >= 0) break;
+        if ((spin & 1023u) == 1023u) {     // a barrier that cannot complete (a counter out of
+          unsigned long long t;             // step with the host copy) traps after 10 s instead
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));   // of hanging the device
+          if (t - t_begin > 10000000000ull) __trap();
+        }
       }
       if (fenced) __threadfence();
     }
@@ -381,9 +389,9 @@ MaintGrid maint_coop_grid(int d) {
 }
 
 template <typename T>
-void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
-                  cudaStream_t st) {
-  if (it.n_staged <= 0 && it.n_chunk <= 0) return;
+cudaError_t launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
+                         cudaStream_t st) {
+  if (it.n_staged <= 0 && it.n_chunk <= 0) return cudaSuccess;
   const MaintGrid mg = maint_coop_grid<T>(g.d);
   it.rows_per_block = mg.rows_per_block;
   const size_t smem = maint_coop_smem<T>(g.d, mg.rows_per_block);
@@ -400,7 +408,8 @@ void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T
       cudaMemcpyToSymbol(g_maint_trace, &trace, sizeof(trace));
     }
   }
-  cudaLaunchCooperativeKernel(kern, dim3(mg.blocks), dim3(kCoopThreads), args, smem, st);
+  const cudaError_t rc = cudaLaunchCooperativeKernel(kern, dim3(mg.blocks), dim3(kCoopThreads), args, smem, st);
+  if (rc != cudaSuccess) return rc;
   if (trace_on && ++trace_n == trace_on) {     // dump the n-th launch: per-block marks, ns
     std::vector<unsigned long long> h((size_t)mg.blocks * 8);
     cudaStreamSynchronize(st);
@@ -413,6 +422,7 @@ void launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T
       std::fprintf(stderr, "%d %llu %llu %llu %llu %llu %llu\n", b, h[b * 8] - t0, h[b * 8 + 1] - t0,
                    h[b * 8 + 2] - t0, h[b * 8 + 3] - t0, h[b * 8 + 4] - t0, h[b * 8 + 5] - t0);
   }
+  return cudaSuccess;
 }
 
 template <typename T>
@@ -424,11 +434,11 @@ int maint_barriers(const Geometry& g, const MaintItems& it) {
   return (int)(rounds > 0 ? 2 * rounds - 1 : 0) * mg.blocks;
 }
 
-template void launch_maint<float>(const Geometry&, const PlanDev&, MaintItems, StateDev<float>, const float*,
+template cudaError_t launch_maint<float>(const Geometry&, const PlanDev&, MaintItems, StateDev<float>, const float*,
                                   cudaStream_t);
 template int maint_barriers<float>(const Geometry&, const MaintItems&);
 template int maint_barriers<__nv_bfloat16>(const Geometry&, const MaintItems&);
-template void launch_maint<__nv_bfloat16>(const Geometry&, const PlanDev&, MaintItems, StateDev<__nv_bfloat16>,
+template cudaError_t launch_maint<__nv_bfloat16>(const Geometry&, const PlanDev&, MaintItems, StateDev<__nv_bfloat16>,
                                           const float*, cudaStream_t);
 
 __global__ void positions_kernel(Geometry g, int32_t* __restrict__ pe) {
