@@ -1,24 +1,34 @@
 """Benchmark of the Cascading KV Cache hot path (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg3|cfg2|cfg5] [--layers L] [--streams S] [--shard-of W]
 
-One STEP = one strided prefill of the whole synthetic sequence through one layer
-(Alg. 1, rows a1-a7 of SURVEY.md section 8, plus the NCCL gather of outputs a9 when N > 1):
-1M tokens through a 65K cascade cache (64 sinks, N = 8 sub-caches, stride 4096, Llama-3-8B
-attention shape: 32 q-heads / 8 kv-heads, d = 128, bf16) -- BASELINE.json configs[2].
-Each step starts from an empty cache (cascade_reset, inside the timed region).  Inputs
-(12.9 GB of Q/K/V) are generated on the device before timing; they exceed the 126 MB L2,
-so no flush is needed between steps.  Row a8 (decode) is measured in the same run on
-configs[3] (64 sequences x 16K cache) and reported under "decode".
+One STEP = one strided prefill of the whole synthetic sequence through every layer of the
+workload (Alg. 1, rows a1-a7 of SURVEY.md section 8, plus the NCCL gather of outputs a9 when
+N > 1).  Default workload (configs[2]): 1M tokens through a 65K cascade cache (64 sinks,
+N = 8 sub-caches, stride 4096, Llama-3-8B attention shape: 32 q-heads / 8 kv-heads, d = 128,
+bf16), one layer.  --workload cfg5 (configs[4]): the same through 32 independent layers, the
+layers' chunks issued chunk-major on S concurrent streams (default 4).  Each step starts from
+empty caches (cascade_reset, inside the timed region).  Inputs are generated on the device
+before timing (seeded per layer; when L distinct input sets do not fit in HBM the layers cycle
+over as many sets as fit -- every layer still computes its own cascade); they exceed the 126 MB
+L2, so no flush is needed between steps.  Row a8 (decode) is measured in the same run on
+configs[3] (64 sequences x 16K cache, state from a real GPU prefill of the 128K prefix) and
+reported under "decode".
 
-N > 1: one process per GPU (torchrun), kv-head sharding (rank r owns kv-heads
-[r*8/N, (r+1)*8/N) and their q-heads, independent cascades), outputs gathered with
-NCCL all_gather per chunk on a side stream.  Total work is fixed -> "scaling": "strong".
-The time is the max over ranks of the device-timed K steps.
+N > 1 (torchrun, one process per GPU): prefill is kv-head sharded (rank r owns kv-heads
+[r*Hkv/N, (r+1)*Hkv/N) and their q-heads; independent cascades) and each (layer, chunk)
+output shard is all_gathered with NCCL on a side stream; decode is batch sharded (64/N
+sequences per rank), its per-step outputs all_gathered the same way.  Total work is
+fixed -> "scaling": "strong".  Times are the max over ranks of the device-timed K steps.
 
---impl reference times the fp64 CPU oracle (oracle/) on the host cores: each step is a
-bounded sample (the first 4096-token chunk of the same workload), scaled to the full
-workload by its measured cost per (query, key) pair.
+--shard-of W (N = 1): runs rank 0's shard of a W-rank job (Hq/W q-heads, Hkv/W kv-heads) on one
+GPU -- the per-rank shapes of the scaling run, measured without the collective.
+
+--impl reference times the fp64 CPU oracle (oracle/) on the host cores, rank 0 only: each step
+is one steady-state chunk (the oracle's cascade filled by score injection to chunk 128) for one
+q-head, scaled to the whole workload by its measured cost per (query, key) pair; the pair
+count comes from the oracle's own Alg. 2 counters.
 """
 
 from __future__ import annotations
@@ -36,7 +46,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "prefill tok/s at 1M ctx, 65K cascade cache; decode tok/s; % TC/HBM peak"
-
 
 T_START = time.time()
 
@@ -60,6 +69,9 @@ WORKLOADS = {
                  "synthetic prefill through a 65K cascade cache (64 sinks + 8 x 8192), stride 4096"),
     "cfg2": dict(name="cfg2_llama8b_4k", desc="configs[1]: Llama-3-8B attention layer, 32K prefill, "
                  "4K cascade cache (64 sinks + 4 x 1024), stride 1024"),
+    "cfg5": dict(name="cfg5_8gpu_32l", desc="configs[4]: 32 independent Llama-3-8B attention layers, 1M-token "
+                 "passkey-shaped synthetic prefill through a 65K cascade cache each (64 sinks + 8 x 8192), "
+                 "stride 4096, head-sharded across the ranks"),
 }
 
 
@@ -107,122 +119,184 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def host_pairs(spec, Hq):
-    """Visible (query, key) pairs per head summed over the run, from the host mirror schedule."""
-    from paper_2406_17808_b200 import cascade as C
-    cfg = C.CascadeConfig(sink_size=spec["sink_size"], cache_size=spec["cache_size"],
-                          num_cascades=spec["num_cascades"], max_stride=spec["stride"])
-    mr = C.Mirror()
+# ---------------------------------------------------------------------------------------------
+# oracle legs (the reference arm and the cpu_baseline): test infrastructure, never the product
+# ---------------------------------------------------------------------------------------------
+
+def oracle_pairs(spec):
+    """Visible (query, key) pairs per q-head of one layer over the whole run, from the ORACLE's
+    own Alg. 2 counters (oracle.cascade.CascadeHead, payload-free tokens): sum over chunks of
+    m * n_resident + m (m + 1) / 2."""
+    from oracle.cascade import CascadeHead, Token
+    head = CascadeHead(spec["sink_size"], spec["cache_size"], spec["num_cascades"])
     m, T = spec["stride"], spec["tokens"]
     pairs = 0
     for start in range(0, T, m):
         mm = min(m, T - start)
-        n_c = mr.sink_count + sum(mr.counts[: spec["num_cascades"]])
-        pairs += mm * n_c + mm * (mm + 1) // 2
-        C.mirror_advance(cfg, mr, mm, want_pe=False, want_ops=False)
-    return pairs * Hq
+        pairs += mm * head.n_resident() + mm * (mm + 1) // 2
+        for t in range(start, start + mm):
+            head.add_token(Token(origin=t))
+        head.events.clear()
+    return pairs
 
 
-def oracle_sample(spec, n_chunks=1):
-    """Times the fp64 oracle (as it stands) on the first n_chunks chunks of the workload.
-    Returns (seconds, pairs processed, tokens processed, threads)."""
-    import numpy as np
-    import torch
-    from oracle.model import CascadeOracle, OracleConfig
-    from paper_2406_17808_b200.synth import Synth, config_seed
-    oc = OracleConfig(1, spec["batch"], spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"],
-                      spec["sink_size"], spec["cache_size"], spec["num_cascades"], rope_theta=spec["rope_theta"],
-                      round_operands="bf16")
-    syn = Synth(spec["batch"], spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"],
-                config_seed(int(spec["key"][3])), eps=spec["eps"])
-    orc = CascadeOracle(oc)
-    m = spec["stride"]
-    chunks = [syn.chunk(c * m, m) for c in range(n_chunks)]
-    pairs = 0
-    t0 = time.perf_counter()
-    for c, (q, k, v) in enumerate(chunks):
-        n_c = orc.heads[0][0][0].n_resident()
-        pairs += spec["num_q_heads"] * spec["batch"] * (m * n_c + m * (m + 1) // 2)
-        f = lambda t: t.to(torch.float64).numpy()
-        orc.prefill_stride(0, f(q), f(k), f(v))
-    dt = time.perf_counter() - t0
-    return dt, pairs, n_chunks * m, len(os.sched_getaffinity(0))
+class OracleSampler:
+    """The fp64 oracle (as it stands) on one q-head / kv-head pair of the workload,
+    its cascade filled to a steady-state occupancy by score injection; each sample() runs the
+    oracle's strided-prefill step on the next chunk and returns (seconds, pairs)."""
+
+    def __init__(self, spec, fill_chunks=128):
+        import numpy as np
+        import torch
+        from oracle.model import CascadeOracle, OracleConfig
+        from paper_2406_17808_b200.synth import Synth, config_seed
+        self.np, self.torch = np, torch
+        G = 1        # one q-head of one kv-head: the per-pair cost is what is measured (bounded sample)
+        self.G, self.m = G, spec["stride"]
+        fill_chunks = min(fill_chunks, spec["tokens"] // self.m - 8)
+        self.orc = CascadeOracle(OracleConfig(1, 1, G, 1, spec["head_dim"], spec["sink_size"], spec["cache_size"],
+                                              spec["num_cascades"], rope_theta=spec["rope_theta"],
+                                              round_operands="bf16"))
+        self.syn = Synth(1, G, 1, spec["head_dim"], config_seed(int(spec["key"][3])), eps=spec["eps"])
+        t0 = time.perf_counter()
+        S = self.orc.cfg.s_tot
+        for c in range(fill_chunks):
+            _, k, v = self.syn.chunk(c * self.m, self.m)
+            f = k.to(torch.float64).numpy()
+            s = np.zeros((1, 1, S + self.m))
+            self.orc.update_with_scores(0, f, v.to(torch.float64).numpy(), s)
+        self.next = fill_chunks
+        self.fill_s = time.perf_counter() - t0
+        self.threads = len(os.sched_getaffinity(0))
+
+    def n_cached(self):
+        return self.orc.heads[0][0][0].n_resident()
+
+    def sample(self):
+        q, k, v = self.syn.chunk(self.next * self.m, self.m)
+        self.next += 1
+        n_c = self.n_cached()
+        pairs = self.G * (self.m * n_c + self.m * (self.m + 1) // 2)
+        f = lambda t: t.to(self.torch.float64).numpy()
+        q, k, v = f(q), f(k), f(v)
+        t0 = time.perf_counter()
+        self.orc.prefill_stride(0, q, k, v)
+        return time.perf_counter() - t0, pairs
 
 
-def run_reference(args, spec, wl):
+def run_reference(args, spec, wl, layers):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    total_pairs = host_pairs(spec, spec["num_q_heads"])
+    total_pairs = oracle_pairs(spec) * spec["num_q_heads"] * layers
+    smp = OracleSampler(spec)
+    log(f"oracle filled to n_cached {smp.n_cached()} in {smp.fill_s:.1f} s")
     for _ in range(args.warmup):
-        oracle_sample(spec)
+        smp.sample()
     secs, pairs = 0.0, 0
     for _ in range(args.steps):
-        dt, p, toks, cores = oracle_sample(spec)
+        dt, p = smp.sample()
         secs += dt
         pairs += p
     per_pair = secs / pairs
     value = spec["tokens"] / (per_pair * total_pairs)
-    sample = (f"first {spec['stride']}-token chunk of the workload (fresh cache) per step, fp64 numpy "
-              f"oracle; scaled to the full run by its measured cost per (query, key) pair "
-              f"({per_pair * 1e9:.3f} ns/pair x {total_pairs:.3e} pairs)")
+    sample = (f"per step: one steady-state {spec['stride']}-token chunk (n_cached ~{smp.n_cached()}) of one "
+              f"q-head / kv-head pair through the fp64 numpy oracle; scaled to the whole "
+              f"workload ({layers} layer(s), {spec['num_q_heads']} q-heads) by its measured cost per (query, key) "
+              f"pair ({per_pair * 1e9:.3f} ns/pair x {total_pairs:.3e} pairs, oracle counters)")
     line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl["desc"]}, "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "oracle",
+            "config": {"workload": wl["desc"], "layers": layers}, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": smp.threads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def decode_bench(args, dev, spec, peaks):
-    """configs[3]: 64 sequences, 16K cascade cache (N=4), single-token steps (row a8)."""
+# ---------------------------------------------------------------------------------------------
+# GPU legs
+# ---------------------------------------------------------------------------------------------
+
+def decode_bench(args, dev, spec, peaks, world, rank, comm, use_dist):
+    """configs[3]: 64 sequences, 16K cascade cache (N = 4), single-token steps (row a8).  The
+    state is a real GPU prefill of each sequence's 128K-token prefix.  N > 1: the sequences are
+    split across the ranks and every step's outputs all_gathered on a side stream."""
     import torch
+    import torch.distributed as dist
     from paper_2406_17808_b200 import cascade as C
     from paper_2406_17808_b200.synth import Synth, config_seed
-    B, m = spec["batch"], spec["stride"]
+    B_all, m = spec["batch"], spec["stride"]
+    if B_all % world:
+        return {"error": f"{B_all} sequences do not split over {world} ranks"}
+    B = B_all // world
     cfg = C.CascadeConfig(batch=B, num_q_heads=spec["num_q_heads"], num_kv_heads=spec["num_kv_heads"],
                           head_dim=spec["head_dim"], sink_size=spec["sink_size"], cache_size=spec["cache_size"],
                           num_cascades=spec["num_cascades"], max_stride=m, dtype="bf16",
                           rope_theta=spec["rope_theta"])
     cas = C.Cascade(cfg, device=dev)
-    syn = Synth(B, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, config_seed(4), eps=spec["eps"])
-    # Decode state: score-injected replay of the 128K-token prefix (k, v synthetic; per-key
-    # mass drawn at random) -- fills the cache exactly as a prefill would; only n_cached
-    # matters for decode throughput.
-    g = torch.Generator(device="cuda").manual_seed(4)
-    for start in range(0, spec["tokens"], m):
-        _, k, v = syn.chunk(start, m, device="cuda")
-        s = torch.rand((B, cfg.num_kv_heads, cfg.s_tot + m), generator=g, device="cuda") * 1e-4
-        cas.update_with_scores(0, k, v, s)
+    syn = Synth(B_all, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, config_seed(4), eps=spec["eps"])
+    bs = slice(rank * B, (rank + 1) * B)
+    t0 = time.time()
+    for start in range(0, spec["tokens"], m):          # real prefill of the 128K prefix
+        q, k, v = syn.chunk(start, m, device="cuda")
+        cas.prefill_stride(0, q[bs].contiguous(), k[bs].contiguous(), v[bs].contiguous())
+    torch.cuda.synchronize()
+    log(f"decode state: real prefill of {B} x {spec['tokens']} tokens in {time.time() - t0:.1f} s")
     steps = spec["decode_steps"]
     qs, ks, vs = [], [], []
     for i in range(steps):
         q, k, v = syn.chunk(spec["tokens"] + i, 1, device="cuda")
-        qs.append(q[:, 0].contiguous()); ks.append(k[:, 0].contiguous()); vs.append(v[:, 0].contiguous())
-    out = torch.empty_like(qs[0])
+        qs.append(q[bs, 0].contiguous()); ks.append(k[bs, 0].contiguous()); vs.append(v[bs, 0].contiguous())
+    R = 4
+    outs = [torch.empty_like(qs[0]) for _ in range(R)]
+    gath = [torch.empty((world,) + tuple(qs[0].shape), dtype=qs[0].dtype, device="cuda") for _ in range(R)] \
+        if use_dist else None
+    ev_free = [None] * R
+    main = torch.cuda.current_stream()
     torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
     cas.profile_enable(True)
     cas.profile_read()
     n0 = cas.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(steps):
-        cas.decode(0, qs[i], ks[i], vs[i], out=out)
+        o = outs[i % R]
+        if ev_free[i % R] is not None:
+            main.wait_event(ev_free[i % R])
+        cas.decode(0, qs[i], ks[i], vs[i], out=o)
+        if use_dist:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                dist.all_gather_into_tensor(gath[i % R].view(-1), o.view(-1))
+                fe = torch.cuda.Event()
+                fe.record(comm)
+            ev_free[i % R] = fe
+    if use_dist:
+        main.wait_stream(comm)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if use_dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     prof = cas.profile_read()
     st = cas.state(0)
     n_c = st["n_cached"]
     bytes_per_step = B * cfg.num_kv_heads * (n_c + 1) * (4 * cfg.head_dim + 20)
     res = {"workload": "configs[3]: 64 sequences x 128K context through a 16K cascade cache "
                        "(64 sinks + 4 x 4096), GQA 32q/8kv d=128 bf16, single-token steps; state "
-                       "from a score-injected replay of the 128K prefix",
-           "value": B * steps / (ms / 1e3), "unit": "tok/s", "steps": steps, "ms_per_step": ms / steps,
+                       "from a real GPU prefill of the 128K prefix (stride 4096)",
+           "value": B_all * steps / (ms / 1e3), "unit": "tok/s", "steps": steps, "ms_per_step": ms / steps,
            "n_cached": n_c, "launches_per_step": (cas.launch_count() - n0) / steps,
-           "hbm_algorithmic_bytes_per_step": bytes_per_step,
+           "parallelism": f"batch sharding x{world} ({B} sequences per rank, NCCL all_gather of every step's outputs)"
+                          if use_dist else "1 GPU",
+           "hbm_algorithmic_bytes_per_step_per_rank": bytes_per_step,
            "hbm_frac": bytes_per_step / (ms / steps / 1e3) / (peaks["hbm"] * 1e9)}
     res["kernels_ms_per_step"] = {k: v[0] / steps for k, v in prof.items() if v[1]}
     cas.close()
@@ -236,6 +310,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=list(WORKLOADS))
+    ap.add_argument("--layers", type=int, default=0, help="override the workload's layer count")
+    ap.add_argument("--streams", type=int, default=0, help="concurrent layer streams (default min(L, 4))")
+    ap.add_argument("--shard-of", type=int, default=1, help="N = 1: run rank 0's shard of a W-rank job")
     ap.add_argument("--tokens", type=int, default=0, help="override sequence length (debug only)")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -248,8 +325,9 @@ def main():
     spec = dict(CONFIGS[wl["name"]], key=wl["name"])
     if args.tokens:
         spec["tokens"] = args.tokens
+    L = args.layers or spec["num_layers"]
     if args.impl == "reference":
-        run_reference(args, spec, wl)
+        run_reference(args, spec, wl, L)
         return
 
     import torch
@@ -261,59 +339,90 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # under torchrun (RANK set) the NCCL path runs even at world size 1 (the gathers are then
+    # one-rank all_gathers: the same code path on one GPU); plain `python bench.py` has none
+    use_dist = "RANK" in os.environ
     torch.cuda.set_device(local)
-    if world > 1:
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
 
     Hq, Hk, d = spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"]
-    q_sl, k_sl = shard_range(rank, world, Hq, Hk)          # kv-head sharding (independent heads)
+    emu = args.shard_of if world == 1 else 1                # per-rank shape emulated on one GPU
+    q_sl, k_sl = shard_range(rank, world * emu, Hq, Hk)     # kv-head sharding (independent heads)
     hq, hk = q_sl.stop - q_sl.start, k_sl.stop - k_sl.start
     m, T, B = spec["stride"], spec["tokens"], spec["batch"]
     nchunks = (T + m - 1) // m
-    cfg = C.CascadeConfig(batch=B, num_q_heads=hq, num_kv_heads=hk, head_dim=d,
+    S = args.streams or min(L, 4)
+    cfg = C.CascadeConfig(num_layers=L, batch=B, num_q_heads=hq, num_kv_heads=hk, head_dim=d,
                           sink_size=spec["sink_size"], cache_size=spec["cache_size"],
                           num_cascades=spec["num_cascades"], max_stride=m, dtype="bf16",
                           rope_theta=spec["rope_theta"])
     cas = C.Cascade(cfg, device=local)
 
-    # ---- inputs, generated on the device (full heads, then this rank's shard) ----
-    seed = config_seed(int(spec["key"][3]))
-    syn = Synth(B, Hq, Hk, d, seed, eps=spec["eps"],
-                passkey_depth=passkey_depth(seed, T) if spec.get("passkey") else None)
-    Q = torch.empty((nchunks, B, m, hq, d), dtype=torch.bfloat16, device="cuda")
-    K = torch.empty((nchunks, B, m, hk, d), dtype=torch.bfloat16, device="cuda")
-    V = torch.empty_like(K)
-    for c in range(nchunks):
-        q, k, v = syn.chunk(c * m, m, device="cuda")
-        Q[c].copy_(q[:, :, q_sl])
-        K[c].copy_(k[:, :, k_sl])
-        V[c].copy_(v[:, :, k_sl])
-    log(f"inputs ready: {nchunks} chunks of {m}")
-    O = torch.empty_like(Q)
-    O_full = torch.empty((nchunks, world, B, m, hq, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
-    comm = torch.cuda.Stream() if world > 1 else None
-    main_stream = torch.cuda.current_stream()
+    # ---- inputs, generated on the device (full heads, then this rank's shard), per layer seed ----
+    set_bytes = 2 * nchunks * B * m * (hq + 2 * hk) * d
+    free = torch.cuda.mem_get_info()[0]
+    n_sets = max(1, min(L, int((free * 0.6) // set_bytes)))
+    sets = []
+    for si in range(n_sets):
+        seed = config_seed(int(spec["key"][3]), si)
+        syn = Synth(B, Hq, Hk, d, seed, eps=spec["eps"],
+                    passkey_depth=passkey_depth(seed, T) if spec.get("passkey") else None)
+        Q = torch.empty((nchunks, B, m, hq, d), dtype=torch.bfloat16, device="cuda")
+        K = torch.empty((nchunks, B, m, hk, d), dtype=torch.bfloat16, device="cuda")
+        V = torch.empty_like(K)
+        for c in range(nchunks):
+            q, k, v = syn.chunk(c * m, m, device="cuda")
+            Q[c].copy_(q[:, :, q_sl])
+            K[c].copy_(k[:, :, k_sl])
+            V[c].copy_(v[:, :, k_sl])
+        sets.append((Q, K, V))
+    log(f"inputs ready: {n_sets} input set(s) for {L} layer(s), {nchunks} chunks of {m}")
+    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(S - 1)]
+    comm = torch.cuda.Stream() if use_dist else None
+    R = 3                                                   # output ring per stream
+    outs = [[torch.empty((B, m, hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(R)] for _ in range(S)]
+    gath = [[torch.empty((world, B, m, hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(R)]
+            for _ in range(S)] if use_dist else None
     torch.cuda.synchronize()
 
+    ev_free = [[None] * R for _ in range(S)]   # per output slot: the gather that last read it
+    slot = [0] * S
+
     def step():
-        cas.reset(0)
+        for l in range(L):
+            cas.reset(l, stream=streams[l % S])
         for c in range(nchunks):
-            cas.prefill_stride(0, Q[c], K[c], V[c], out=O[c])
-            if world > 1:
-                ev = torch.cuda.Event()
-                ev.record(main_stream)
-                comm.wait_event(ev)
-                with torch.cuda.stream(comm):
-                    gather_heads(O[c], world, buf=O_full[c])
-        if world > 1:
-            main_stream.wait_stream(comm)
+            for l in range(L):
+                si = l % S
+                st = streams[si]
+                Q, K, V = sets[l % n_sets]
+                r = slot[si]
+                slot[si] = (r + 1) % R
+                if ev_free[si][r] is not None:
+                    st.wait_event(ev_free[si][r])
+                o = outs[si][r]
+                cas.prefill_stride(l, Q[c], K[c], V[c], out=o, stream=st)
+                if use_dist:
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    comm.wait_event(ev)
+                    with torch.cuda.stream(comm):
+                        gather_heads(o, world, buf=gath[si][r], assemble=False)   # no reshape copy
+                        fe = torch.cuda.Event()
+                        fe.record(comm)
+                    ev_free[si][r] = fe
+        for st in streams[1:]:
+            streams[0].wait_stream(st)
+        if use_dist:
+            streams[0].wait_stream(comm)
 
     for i in range(args.warmup):
         step()
         torch.cuda.synchronize()
         log(f"warmup step {i} done")
-    if world > 1:
+    if use_dist:
         dist.barrier()
 
     clocks = ClockSampler(local)
@@ -321,7 +430,7 @@ def main():
     cas.profile_enable(True)
     cas.profile_read()
     n0 = cas.launch_count()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -330,7 +439,7 @@ def main():
         step()
     e1.record()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
     log(f"timed {args.steps} steps: {ms:.1f} ms")
@@ -338,7 +447,7 @@ def main():
     prof = cas.profile_read()
     cas.profile_enable(False)
     clk = clocks.stop()
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -357,100 +466,119 @@ def main():
     r1, t1, c1, w1 = rate("attn_fwd")
     r2, t2, c2, w2 = rate("attn_score")
     rm, tm, cm, wm = rate("maintenance")
+    concurrent = S > 1
     # the attention kernels run inside a seconds-long, power-capped step: the roofline peak is
     # the SUSTAINED bf16 figure (MEASURED_PEAKS.json bf16_tflops_sustained); burst reported beside
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01_v11.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")) as f:
             traffic = json.load(f)["attn_fwd"]["dram_bytes_per_launch"]
     except Exception:
         pass
     roof = {"kernel": "attn_fwd (pass 1: O and LSE over [sinks | cascade | chunk])", "bound": "tensor",
             "achieved": r1 / 1e12, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
             "frac": r1 / 1e12 / peaks["bf16_sus"], "frac_of_burst": r1 / 1e12 / peaks["bf16"],
-            "traffic": traffic, "traffic_note": "dram read+write bytes of one steady-state launch "
-            "(n_cached 62463), profiles/ncu_traffic_r01_v11.json",
+            "traffic": traffic if not emu > 1 and L == 1 else None,
+            "traffic_note": "dram read+write bytes of one steady-state launch, profiles/ncu_traffic_r02.json",
             "peak_source": peaks["src"] + " bf16 dense, sustained (kernel timed inside a long step)",
             "work": "4*d flops per visible (query, key) pair"}
+    if concurrent:
+        roof["note"] = (f"{S} concurrent layer streams: each launch's event span includes time the SMs spend on "
+                        "other streams' kernels, so frac is a lower bound")
     extra_roof = {
-        "attention_total": {"kernels": "attn_fwd + attn_score", "achieved": w1 / ((t1 + t2) / 1e3) / 1e12 if t1 + t2 > 0 else 0,
+        "attention_total": {"kernels": "attn_fwd + attn_score",
+                            "achieved": w1 / ((t1 + t2) / 1e3) / 1e12 if t1 + t2 > 0 else 0,
                             "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                            "frac": (w1 / ((t1 + t2) / 1e3) / 1e12 / peaks["bf16_sus"]) if t1 + t2 > 0 else 0},
+                            "frac": (w1 / ((t1 + t2) / 1e3) / 1e12 / peaks["bf16_sus"]) if t1 + t2 > 0 else 0,
+                            "frac_of_burst": (w1 / ((t1 + t2) / 1e3) / 1e12 / peaks["bf16"]) if t1 + t2 > 0 else 0},
         "maintenance": {"kernel": "maint_coop_kernel (Alg. 2 admission, selections, K/V/mu/origin moves; "
                                   "the EMA fold runs in attn_score's epilogue)",
                         "bound": "hbm", "achieved": rm / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": rm / 1e9 / peaks["hbm"],
-                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)",
-                        "note": "event-timed per launch: includes ~5 us of launch + event edge per launch "
-                                "(profiles/launch_edge_r01.txt); the kernel's own span streams at ~69 % "
-                                "(DESIGN.md, Cache maintenance)"},
+                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)"},
+        "step_useful": {"achieved": w1 / args.steps / (ms_step / 1e3) / 1e12, "unit": "TFLOP/s",
+                        "note": "useful attention flops per step / whole step time (every kernel, all streams)"},
     }
     share = {k: v["ms_per_step"] / ms_step for k, v in kern.items()}
-
+    par = (f"kv-head sharding x{world} (NCCL all_gather of outputs)" if use_dist else
+           (f"rank 0 of a {emu}-rank kv-head sharding, emulated on 1 GPU" if emu > 1 else "1 GPU"))
     result = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
               "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
               "config": {"workload": wl["desc"], "tokens": T, "batch": B, "stride": m,
                          "cache": spec["cache_size"], "sinks": spec["sink_size"],
-                         "cascades": spec["num_cascades"], "heads": f"{Hq}q/{Hk}kv d={d}", "layers": 1,
-                         "parallelism": f"kv-head sharding x{world}" if world > 1 else "1 GPU",
-                         "l2": "inputs (12.9 GB) and cache state exceed L2; no flush needed"},
+                         "cascades": spec["num_cascades"], "heads": f"{Hq}q/{Hk}kv d={d}",
+                         "heads_per_rank": f"{hq}q/{hk}kv", "layers": L, "layer_streams": S,
+                         "distinct_input_sets": n_sets, "parallelism": par,
+                         "l2": "inputs and cache state exceed L2; no flush needed"},
               "roofline": roof, "roofline_other": extra_roof, "kernels": kern, "kernel_share": share,
               "gpu_launches": launches, "clocks": clk}
+    if use_dist:
+        result["collective"] = {"op": "all_gather_into_tensor (NCCL) of every (layer, chunk) output shard",
+                                "bytes_per_step_per_rank": 2 * B * m * hq * d * nchunks * L}
 
     # ---- e2e: host (pinned) buffers through cascade_prefill_stride_host_async ----
     # (every chunk's q/k/v go host->device and its output device->host inside the timed region;
     # the library overlaps those copies with the neighbouring chunks' compute)
     if not args.no_e2e:
         log("e2e start")
+        Q, K, V = sets[0]
         Qh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
         Kh = torch.empty(K.shape, dtype=K.dtype, pin_memory=True)
         Vh = torch.empty(V.shape, dtype=V.dtype, pin_memory=True)
-        Oh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+        Oh = torch.empty((2 * L,) + tuple(Q.shape[1:]), dtype=Q.dtype, pin_memory=True)
         Qh.copy_(Q); Kh.copy_(K); Vh.copy_(V)
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        cas.reset(0)
+        for l in range(L):
+            cas.reset(l)
         for c in range(nchunks):
-            cas.prefill_stride_host_async(0, Qh[c], Kh[c], Vh[c], Oh[c])
+            for l in range(L):
+                # outputs: a ring of 2 L host slots; the library's two staging sets alternate per
+                # call and a slot is reused only two calls per layer later (its copy is done)
+                cas.prefill_stride_host_async(l, Qh[c], Kh[c], Vh[c], Oh[(c % 2) * L + l])
         cas.host_wait()                      # every output is in host memory
         f1.record()
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
-        if world > 1:
+        if use_dist:
             t = torch.tensor([ems], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        h2d = (Q.numel() + K.numel() + V.numel()) * 2 * world
-        result["e2e"] = {"value": T * B / (ems / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
-                         "d2h_bytes_per_step": O.numel() * 2 * world,
+        per_call_in = (Q[0].numel() + K[0].numel() + V[0].numel()) * 2
+        result["e2e"] = {"value": T * B / (ems / 1e3), "unit": "tok/s",
+                         "h2d_bytes_per_step": per_call_in * nchunks * L * world,
+                         "d2h_bytes_per_step": Q[0].numel() * 2 * nchunks * L * world,
                          "api": "cascade_prefill_stride_host_async + cascade_host_wait (pinned host q/k/v/out; "
-                                "copies on library streams, overlapped with compute)"}
+                                "copies on library streams, overlapped with compute; layers in call order)"}
         del Qh, Kh, Vh, Oh
 
-    del Q, K, V, O, O_full
+    del sets, outs, gath
+    cas.close()
     torch.cuda.empty_cache()
-    log("decode start")
-    if rank == 0 and not args.no_decode and world == 1:
+    if not args.no_decode and emu == 1:
+        log("decode start")
         try:
-            result["decode"] = decode_bench(args, local, dict(CONFIGS["cfg4_decode"]), peaks)
+            result["decode"] = decode_bench(args, local, dict(CONFIGS["cfg4_decode"]), peaks, world, rank, comm, use_dist)
         except Exception as e:   # reported, never hidden
             result["decode"] = {"error": repr(e)}
-    log("cpu baseline start")
-    if rank == 0 and not args.no_cpu:
-        secs, pairs, toks, cores = oracle_sample(spec)
-        total_pairs = host_pairs(spec, Hq)
+    if rank == 0 and not args.no_cpu and world == 1:
+        log("cpu baseline start")
+        smp = OracleSampler(spec)
+        secs, pairs = smp.sample()
+        total_pairs = oracle_pairs(spec) * Hq * L
         per_pair = secs / pairs
         result["cpu_baseline"] = {
-            "value": T * B / (per_pair * total_pairs), "unit": "tok/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {m}-token chunk ({pairs:.3e} pairs) timed in {secs:.1f} s; scaled by "
-                      f"cost per (query, key) pair to the run's {total_pairs:.3e} pairs"}
+            "value": T * B / (per_pair * total_pairs), "unit": "tok/s", "cores": smp.threads, "kind": "oracle",
+            "sample": f"one steady-state {m}-token chunk (n_cached {smp.n_cached()}) of one q-head "
+                      f"({pairs:.3e} pairs) timed in {secs:.1f} s after a {smp.fill_s:.1f} s score-injection "
+                      f"fill; scaled by cost per (query, key) pair to the run's {total_pairs:.3e} pairs"}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

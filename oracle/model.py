@@ -164,6 +164,9 @@ class CascadeOracle:
     def update_with_scores(self, layer: int, k: np.ndarray, v: np.ndarray, s_flat: np.ndarray) -> None:
         """Score injection: fold the given s [B,Hkv,S_tot+m] and insert k/v [B,m,Hkv,d]."""
         cfg = self.cfg
+        if cfg.head_policy == "homogeneous" and cfg.head_reduce == "median":
+            # the median of all q-heads (P:542) is not a function of the kv-head scores given here
+            raise ValueError("homogeneous + median needs per-q-head masses; score injection has per-kv-head s")
         s_flat = np.asarray(s_flat, dtype=np.float64)
         for b in range(cfg.batch):
             s_b = s_flat[b]

@@ -120,7 +120,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.maint_ctl = align_up(8 + 8 * B * Hk);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
                 z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_ctl;
-  z.rope_tab = align_up((S + M) * (d / 2) * sizeof(float2));
+  z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(float2));
   z.tab_lo = align_up(32 * (d / 2) * sizeof(float2));
   z.stage_q = align_up(B * M * Hq * d * es);
@@ -142,7 +142,7 @@ struct cascade_handle {
   std::vector<LayerBufs> layers;
   std::vector<cascade_mirror> mirrors;
   std::vector<int32_t> m_last;
-  float2* rope_tab;
+  double2* rope_tab;     // [S_tot + max_stride][d/2] (cos, sin)(pos theta_i) in fp64
   float2* tab_hi;
   float2* tab_lo;
   void *stage_q, *stage_k, *stage_v, *stage_out;           // set 0 (aliases stage[0])
@@ -332,7 +332,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.maint_ctl = reinterpret_cast<uint32_t*>(take(sz.maint_ctl));
     L.maint_barrier = 0;
   }
-  h->rope_tab = reinterpret_cast<float2*>(take(sz.rope_tab));
+  h->rope_tab = reinterpret_cast<double2*>(take(sz.rope_tab));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
   h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
   for (int i = 0; i < 2; ++i) {
@@ -382,19 +382,20 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
            make_map(&L.tm_kraw, L.k_raw, B * Hk * (uint64_t)h->S_tot, d);
     }
   }
-  // RoPE table: (cos, sin)(pos * theta^(-2i/d)) computed in double, rounded to fp32 (Q11).
+  // RoPE table: (cos, sin)(pos * theta^(-2i/d)) in double (Q11); the rotation itself runs in
+  // double too, so the rotated operand rounds to the same bf16 as the exact rotation (Q17)
   {
     const int half = cfg->head_dim / 2;
     const size_t npos = (size_t)h->S_tot + cfg->max_stride;
-    std::vector<float2> tab(npos * half);
+    std::vector<double2> tab(npos * half);
     for (int i = 0; i < half; ++i) {
       const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
       for (size_t pos = 0; pos < npos; ++pos) {
         const double a = (double)pos * f;
-        tab[pos * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+        tab[pos * half + i] = make_double2(std::cos(a), std::sin(a));
       }
     }
-    ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(float2),
+    ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(double2),
                           cudaMemcpyHostToDevice) == cudaSuccess;
     // angle-addition factors for decode: pe = 32 a + b, cos/sin(32 a theta_i) and cos/sin(b theta_i)
     const size_t nhi = npos / 32 + 1;

@@ -72,7 +72,7 @@ struct StateDev {
 // ---- launchers (defined in the .cu files) --------------------------------
 template <typename T>
 void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, const T* k_raw_state,
-                      const float2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st);
+                      const double2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st);
 
 template <typename T>
 void launch_attn_fwd_simt(const Geometry& g, const T* q_rot, const T* k_rot, const T* v_state,
@@ -160,7 +160,7 @@ struct DecodeParams {
   double* mu;                   // state
   int64_t* origin;              // state
   float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
-  const float2* tab;            // [npos][D/2] cos/sin(pe theta_i)
+  const double2* tab;           // [npos][D/2] cos/sin(pe theta_i), fp64
   const float2* tab_hi;         // [npos/32 + 1][D/2] cos/sin(32 a theta_i)
   const float2* tab_lo;         // [32][D/2] cos/sin(b theta_i)
   float* logits;                // [B*Hkv][S_tot + 1][G] log2-domain scaled logits

@@ -106,10 +106,10 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
     float r1 = 0.f, r2 = 0.f;
     if (h < G) {
       const __nv_bfloat16* qp = p.q + ((long long)b * p.Hq + g * G + h) * D;
-      const float2 cs = p.tab[(long long)(p.n_keys - 1) * HALF + i];
-      const float x1 = __bfloat162float(qp[i]), x2 = __bfloat162float(qp[i + HALF]);
-      r1 = x1 * cs.x - x2 * cs.y;
-      r2 = x2 * cs.x + x1 * cs.y;
+      const double2 cs = p.tab[(long long)(p.n_keys - 1) * HALF + i];
+      const double x1 = __bfloat162float(qp[i]), x2 = __bfloat162float(qp[i + HALF]);
+      r1 = __double2float_rn(__dsub_rn(__dmul_rn(x1, cs.x), __dmul_rn(x2, cs.y)));
+      r2 = __double2float_rn(__dadd_rn(__dmul_rn(x2, cs.x), __dmul_rn(x1, cs.y)));
     }
     const int off = h * 128 + ((((i >> 3) ^ (h & 7))) << 4) + (i & 7) * 2;
     *reinterpret_cast<__nv_bfloat16*>(sQ + off) = __float2bfloat16_rn(r1);
@@ -276,11 +276,11 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
 #pragma unroll
               for (int u = 0; u < 2; ++u) {
                 const int i = c * 8 + 2 * e2 + u;
-                const float2 cs = p.tab[(long long)pe * HALF + i];
-                const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
-                const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
-                r[u] = x1 * cs.x - x2 * cs.y;
-                r[2 + u] = x2 * cs.x + x1 * cs.y;
+                const double2 cs = p.tab[(long long)pe * HALF + i];
+                const double x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
+                const double x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
+                r[u] = __double2float_rn(__dsub_rn(__dmul_rn(x1, cs.x), __dmul_rn(x2, cs.y)));
+                r[2 + u] = __double2float_rn(__dadd_rn(__dmul_rn(x2, cs.x), __dmul_rn(x1, cs.y)));
               }
               oa[e2] = tc::pack_bf16(r[0], r[1]);
               ob[e2] = tc::pack_bf16(r[2], r[3]);

@@ -7,7 +7,7 @@
 //                                   rotated to n_cached + r
 //   v_chunk[B][Hkv][ldc][d]         chunk values, head-major
 // Keys are cached pre-RoPE (Q11) because ranks change every chunk.  cos/sin come from a table
-// built on the host in float64 and rounded to fp32 (rope_tab[pos][i]).
+// built on the host in float64 (rope_tab[pos][i]); the rotation runs in float64 (Q17).
 //
 // HBM-bound: every thread moves one 16-byte vector of the first half of a row and the
 // matching vector of the second half (rotate-half pairs (i, i + d/2)), so D/(2*EPV) threads
@@ -49,19 +49,24 @@ template <> struct Vec<__nv_bfloat16> {
   }
 };
 
-// rotate-half on one vector pair: lo = x[i..i+N), hi = x[i+d/2 .. i+d/2+N) at frequencies i..i+N
+// rotate-half on one vector pair: lo = x[i..i+N), hi = x[i+d/2 .. i+d/2+N) at frequencies i..i+N.
+// The rotation runs in double with separately rounded products (never an FMA) and the result is
+// rounded double -> float -> T, the same operations as the oracle's float64 rotation followed by
+// its rounding (reading Q17): the bf16 operand the score products consume is then the oracle's
+// bit for bit, instead of differing by one bf16 ulp whenever a float32 rotation error straddles a
+// rounding midpoint (which moved single per-key masses by percents).
 template <typename T>
-__device__ __forceinline__ void rotate(uint4& lo, uint4& hi, const float2* __restrict__ cs) {
+__device__ __forceinline__ void rotate(uint4& lo, uint4& hi, const double2* __restrict__ cs) {
   constexpr int N = Vec<T>::N;
   float a[N], b[N];
   Vec<T>::unpack(lo, a);
   Vec<T>::unpack(hi, b);
 #pragma unroll
   for (int e = 0; e < N; ++e) {
-    const float2 c = cs[e];
-    const float x1 = a[e], x2 = b[e];
-    a[e] = x1 * c.x - x2 * c.y;
-    b[e] = x2 * c.x + x1 * c.y;
+    const double2 c = cs[e];
+    const double x1 = a[e], x2 = b[e];
+    a[e] = __double2float_rn(__dsub_rn(__dmul_rn(x1, c.x), __dmul_rn(x2, c.y)));
+    b[e] = __double2float_rn(__dadd_rn(__dmul_rn(x2, c.x), __dmul_rn(x1, c.y)));
   }
   lo = Vec<T>::pack(a);
   hi = Vec<T>::pack(b);
@@ -74,7 +79,7 @@ __device__ __forceinline__ void rotate(uint4& lo, uint4& hi, const float2* __res
 template <typename T, typename I>
 __global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __restrict__ q, const T* __restrict__ k,
                                                         const T* __restrict__ v, const T* __restrict__ k_raw,
-                                                        const float2* __restrict__ tab, T* __restrict__ q_rot,
+                                                        const double2* __restrict__ tab, T* __restrict__ q_rot,
                                                         T* __restrict__ k_rot, T* __restrict__ v_chunk) {
   constexpr int N = Vec<T>::N;                 // elements per 16-byte vector
   const int half = g.d >> 1;
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(256) rope_prep_kernel(Geometry g, const T* __r
 
 template <typename T>
 void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, const T* k_raw_state,
-                      const float2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st) {
+                      const double2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st) {
   const int tpr = (g.d / 2) / Vec<T>::N;
   const long long total = ((long long)g.B * g.Hq * g.m + (long long)g.B * g.Hkv * (g.S_tot + g.m) +
                            (long long)g.B * g.Hkv * g.m) * tpr;
@@ -148,9 +153,9 @@ void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, con
 }
 
 template void launch_rope_prep<float>(const Geometry&, const float*, const float*, const float*,
-                                      const float*, const float2*, float*, float*, float*, cudaStream_t);
+                                      const float*, const double2*, float*, float*, float*, cudaStream_t);
 template void launch_rope_prep<__nv_bfloat16>(const Geometry&, const __nv_bfloat16*, const __nv_bfloat16*,
-                                              const __nv_bfloat16*, const __nv_bfloat16*, const float2*,
+                                              const __nv_bfloat16*, const __nv_bfloat16*, const double2*,
                                               __nv_bfloat16*, __nv_bfloat16*, __nv_bfloat16*, cudaStream_t);
 
 }  // namespace cascade

@@ -31,10 +31,16 @@ def shard_range(rank: int, world: int, num_q_heads: int, num_kv_heads: int) -> T
 
 
 def gather_heads(out_shard: torch.Tensor, world: int, buf: torch.Tensor | None = None,
-                 group=None) -> torch.Tensor:
-    """all_gather [B, m, Hq/N, d] shards -> [B, m, Hq, d] (a permuted view of the gather buffer)."""
+                 group=None, assemble: bool = True) -> torch.Tensor:
+    """all_gather [B, m, Hq/N, d] shards into buf [N, B, m, Hq/N, d].
+
+    assemble=True returns the [B, m, Hq, d] tensor in head order (a copy: the gathered layout is
+    rank-major); assemble=False returns the gather buffer itself (no copy), which is what the
+    benchmark's per-chunk gather uses."""
     B, m, hq, d = out_shard.shape
     if buf is None:
         buf = torch.empty((world, B, m, hq, d), dtype=out_shard.dtype, device=out_shard.device)
     dist.all_gather_into_tensor(buf.view(-1), out_shard.contiguous().view(-1), group=group)
+    if not assemble:
+        return buf
     return buf.permute(1, 2, 0, 3, 4).reshape(B, m, world * hq, d)

@@ -1,0 +1,141 @@
+"""GPU parity cases added to close the round-1 gaps: every GQA group size the bf16 path accepts
+(G = 1, 2, 4, 8 and a non-power-of-two 3) through prefill and decode; the configs[4] per-rank
+shape scaled down (4 layers x 1 kv-head, layers interleaved on four streams) against the
+oracle; the unrounded float64 oracle (reading Q17 off) against the GPU; the binding's shape
+checks.  Everything goes through the C ABI."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.model import CascadeOracle, OracleConfig
+from paper_2406_17808_b200 import cascade as C
+from paper_2406_17808_b200.synth import CONFIGS, Synth, config_seed
+
+pytestmark = pytest.mark.gpu
+
+O_TOL, S_RTOL = 2e-2, 1e-3
+
+
+def _np(t):
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def _orc(cfg, **kw):
+    return CascadeOracle(OracleConfig(cfg.num_layers, cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+                                      cfg.sink_size, cfg.cache_size, cfg.num_cascades, gamma=cfg.ema_gamma,
+                                      rope_theta=cfg.rope_theta, round_operands=kw.get("round", "bf16"),
+                                      head_reduce=cfg.head_reduce))
+
+
+def _contents_equal(gpu_st, orc_st, layer_meta=True):
+    np.testing.assert_array_equal(gpu_st["origin"].cpu().numpy(), orc_st["origin"])
+    np.testing.assert_array_equal(np.broadcast_to(gpu_st["pe"].cpu().numpy(), orc_st["origin"].shape),
+                                  orc_st["pe"])
+    meta = orc_st["meta"][0][0]
+    assert (gpu_st["t"], gpu_st["sink_count"], gpu_st["counts"], gpu_st["xi"]) == \
+        (meta["t"], meta["sink_count"], meta["counts"], meta["xi"])
+
+
+@pytest.mark.parametrize("Hq,d,reduce", [(2, 128, "max"), (4, 128, "max"), (16, 128, "max"), (6, 128, "max"),
+                                         (16, 128, "median"), (8, 64, "max"), (4, 64, "mean")])
+def test_gqa_groups_prefill_and_decode(Hq, d, reduce):
+    """Hkv = 2 and Hq in {2, 4, 16, 6, 8}: GQA groups 1, 2, 8, 3 and 4 through the tcgen05
+    prefill passes (pass 2 reduces the group in shared memory) and decode (the dedicated decode
+    kernels for G in {1, 2, 4, 8} at d = 128, the m = 1 strided path otherwise), B = 2, ragged
+    strides, then 24 decode steps; outputs, exact masses and the cascade contents vs the oracle."""
+    cfg = C.CascadeConfig(batch=2, num_q_heads=Hq, num_kv_heads=2, head_dim=d, sink_size=4, cache_size=96,
+                          num_cascades=3, max_stride=160, dtype="bf16", head_reduce=reduce)
+    syn = Synth(2, Hq, 2, d, seed=300 + Hq + d)
+    gpu, orc = C.Cascade(cfg), _orc(cfg)
+    start = 0
+    for m in (160, 37, 128, 1, 150):
+        q, k, v = syn.chunk(start, m)
+        start += m
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        O_ref, s_ref = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL, m
+        np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+        _contents_equal(gpu.state(0), orc.state(0))
+    for step in range(24):
+        q, k, v = syn.chunk(start + step, 1)
+        out = gpu.decode(0, q[:, 0].contiguous().cuda(), k[:, 0].contiguous().cuda(), v[:, 0].contiguous().cuda())
+        O_ref, s_ref = orc.decode(0, _np(q[:, 0]), _np(k[:, 0]), _np(v[:, 0]))
+        torch.cuda.synchronize()
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL, step
+        np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+    _contents_equal(gpu.state(0), orc.state(0))
+    margins = orc.select_margins()
+    assert margins.size > 0 and margins.min() > 1e-3
+
+
+def test_multilayer_single_kvhead_shard_matches_oracle():
+    """configs[4]'s per-rank shape at 8 ranks, scaled down: 4 layers x (4 q-heads, 1 kv-head),
+    each layer with its own seeded inputs, the layers' chunks issued interleaved on four streams
+    (the cfg5 bench drives layers concurrently); every layer's outputs, masses and cascade contents
+    vs a 4-layer oracle."""
+    L, m = 4, 128
+    cfg = C.CascadeConfig(num_layers=L, batch=1, num_q_heads=4, num_kv_heads=1, head_dim=128, sink_size=16,
+                          cache_size=512, num_cascades=4, max_stride=m, dtype="bf16")
+    gpu, orc = C.Cascade(cfg), _orc(cfg)
+    syns = [Synth(1, 4, 1, 128, seed=config_seed(5, l)) for l in range(L)]
+    streams = [torch.cuda.Stream() for _ in range(L)]
+    for c in range(10):
+        chunks = [syns[l].chunk(c * m, m) for l in range(L)]
+        outs = []
+        for l in range(L):
+            q, k, v = (t.cuda() for t in chunks[l])
+            with torch.cuda.stream(streams[l]):
+                outs.append((gpu.prefill_stride(l, q, k, v, stream=streams[l]),
+                             gpu.last_scores(l, stream=streams[l])))
+        torch.cuda.synchronize()
+        for l in range(L):
+            q, k, v = chunks[l]
+            O_ref, s_ref = orc.prefill_stride(l, _np(q), _np(k), _np(v))
+            assert np.abs(_np(outs[l][0]) - O_ref).max() <= O_TOL, (c, l)
+            np.testing.assert_allclose(_np(outs[l][1]), s_ref, rtol=S_RTOL, atol=1e-30)
+    for l in range(L):
+        ost = orc.state(l)
+        np.testing.assert_array_equal(gpu.state(l)["origin"].cpu().numpy(), ost["origin"])
+    assert orc.select_margins().min() > 1e-3
+
+
+def test_unrounded_oracle_also_within_tolerance():
+    """Reading Q17 off: the plain float64 oracle (no bf16 rounding of the rotated operands) on
+    configs[1]'s first chunks is also within the 2e-2 output tolerance of the GPU, and takes the
+    same cascade decisions."""
+    spec = CONFIGS["cfg2_llama8b_4k"]
+    cfg = C.CascadeConfig(batch=1, num_q_heads=32, num_kv_heads=8, head_dim=128, sink_size=64,
+                          cache_size=4096, num_cascades=4, max_stride=1024, dtype="bf16",
+                          rope_theta=spec["rope_theta"])
+    syn = Synth(1, 32, 8, 128, config_seed(2), eps=spec["eps"])
+    gpu, orc = C.Cascade(cfg), _orc(cfg, round="")
+    for c in range(3):
+        q, k, v = syn.chunk(c * 1024, 1024)
+        out = gpu.prefill_stride(0, q.cuda(), k.cuda(), v.cuda())
+        O_ref, _ = orc.prefill_stride(0, _np(q), _np(k), _np(v))
+        assert np.abs(_np(out) - O_ref).max() <= O_TOL
+    np.testing.assert_array_equal(gpu.state(0)["origin"].cpu().numpy(), orc.state(0)["origin"])
+
+
+def test_binding_rejects_mismatched_tensors():
+    """The C ABI takes raw pointers; the binding checks every tensor against the config so a
+    wrong shape or device never reaches the kernels (out-of-bounds reads/writes otherwise)."""
+    cfg = C.CascadeConfig(batch=2, num_q_heads=4, num_kv_heads=2, head_dim=64, sink_size=2, cache_size=8,
+                          num_cascades=2, max_stride=8, dtype="bf16")
+    gpu = C.Cascade(cfg)
+    bf = dict(dtype=torch.bfloat16, device="cuda")
+    q, k = torch.zeros((2, 4, 4, 64), **bf), torch.zeros((2, 4, 2, 64), **bf)
+    with pytest.raises(ValueError):
+        gpu.prefill_stride(0, q, q, k)                               # k with q's head count
+    with pytest.raises(ValueError):
+        gpu.prefill_stride(0, q[:1].contiguous(), k[:1].contiguous(), k[:1].contiguous())   # batch 1 != 2
+    with pytest.raises(ValueError):
+        gpu.prefill_stride(0, q, k, k, out=torch.zeros((2, 4, 4, 32), **bf))
+    with pytest.raises(ValueError):
+        gpu.decode(0, q[:, 0].contiguous(), q[:, 0].contiguous(), k[:, 0].contiguous())
+    with pytest.raises(ValueError):
+        gpu.prefill_stride(0, q.cpu(), k.cpu(), k.cpu())
+    gpu.prefill_stride(0, q, k, k)                                   # the right shapes work
+    assert gpu.state(0)["t"] == 4

@@ -3,10 +3,10 @@ cascade, 64 sinks, N = 8, stride 4096) in the launch configuration bench.py time
 
 * The whole 2^20-token Alg. 2 schedule, score-injected (identical fp32 scores on both sides):
   the cascade state is bit-exact at checkpoints through the last chunk.
-* Sampled attention: the real prefill of all 32 q-heads / 8 kv-heads runs on the GPU; before a
-  sampled chunk the GPU's cascade state is exported, and the oracle recomputes the chunk's
-  attention output and exact per-key mass from that state (keys rotated to their exported rank
-  pe), row block by row block, in float64.
+* The real prefill of all 32 q-heads / 8 kv-heads: the GPU's own per-chunk scores replayed
+  through the oracle's Alg. 2 (every real selection decision, bit-exact state at checkpoints,
+  margin audit), and sampled chunks' attention output and exact per-key mass recomputed by the
+  oracle from the exported state (keys rotated to their exported rank pe), in float64.
 """
 
 import numpy as np
@@ -88,7 +88,19 @@ def _oracle_chunk(st, b, g, q, k, v, heads, gamma, theta, scale, block=512):
     return outs, np.array(masses), order, n_c
 
 
-def test_cfg3_sampled_chunks_match_oracle():
+def test_cfg3_real_run_replayed_by_oracle_and_sampled_chunks():
+    """The real configs[2] run (1M tokens, all 32 q-heads / 8 kv-heads, passkey inputs, the launch
+    configuration bench.py times), checked three ways:
+
+    * replay: after every chunk the GPU's own per-key masses (cascade_last_scores) and the chunk's
+      K/V of kv-heads {0, 7} are fed to the oracle's Alg. 2 (update_with_scores); at checkpoints
+      the GPU state of those heads -- origins, pe, counts, xi, mu bit patterns, K/V bits -- must
+      equal the oracle's bit for bit: every one of the run's real selection decisions is checked;
+    * margin audit: the relative margins of those real decisions (reported; the end-to-end bar of
+      the north star needs > 1e-3);
+    * sampled attention: chunks {0, 16, 128, 255} x kv-groups {0, 7} (q-heads 0-3 and 28-31): the
+      oracle recomputes O and the exact per-key mass from the exported pre-chunk state in float64.
+    """
     B, Hq, Hkv, d, m = SPEC["batch"], SPEC["num_q_heads"], SPEC["num_kv_heads"], SPEC["head_dim"], SPEC["stride"]
     cfg = C.CascadeConfig(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d, sink_size=SPEC["sink_size"],
                           cache_size=SPEC["cache_size"], num_cascades=SPEC["num_cascades"], max_stride=m,
@@ -96,32 +108,58 @@ def test_cfg3_sampled_chunks_match_oracle():
     gpu = C.Cascade(cfg)
     seed = config_seed(3)
     T = SPEC["tokens"]
+    nch = T // m
     syn = Synth(B, Hq, Hkv, d, seed, eps=SPEC["eps"], passkey_depth=passkey_depth(seed, T))
     G = Hq // Hkv
     scale = 1.0 / np.sqrt(d)
-    samples = {16: [(7, [31])], T // m - 1: [(0, [0, 1, 2, 3])]}   # chunk -> [(kv-group, q-heads)]
-    for c in range(T // m):
+    heads_kv = [0, Hkv - 1]
+    rep = CascadeOracle(OracleConfig(1, B, len(heads_kv), len(heads_kv), d, cfg.sink_size, cfg.cache_size,
+                                     cfg.num_cascades, gamma=cfg.ema_gamma))
+    samples = {0, 16, 128, nch - 1}
+    checkpoints = {0, 1, 16, 64, 128, 200, nch - 1}
+    for c in range(nch):
         q, k, v = syn.chunk(c * m, m, device="cuda")
         if c in samples:
             st = gpu.state(0)
         out = gpu.prefill_stride(0, q, k, v)
+        s_gpu = gpu.last_scores(0).cpu().numpy()                     # float32, [B, Hkv, S_tot + m]
+        kc, vc = k.cpu(), v.cpu()
+        rep.update_with_scores(0, _np(kc[:, :, heads_kv]), _np(vc[:, :, heads_kv]),
+                               s_gpu[:, heads_kv].astype(np.float64))
+        if c in checkpoints:
+            gst, ost = gpu.state(0), rep.state(0)
+            o = ost["origin"]
+            np.testing.assert_array_equal(gst["origin"].cpu().numpy()[:, heads_kv], o)
+            np.testing.assert_array_equal(np.broadcast_to(gst["pe"].cpu().numpy(), o.shape), ost["pe"])
+            meta = ost["meta"][0][0]
+            assert (gst["t"], gst["sink_count"], gst["counts"], gst["xi"]) == \
+                (meta["t"], meta["sink_count"], meta["counts"], meta["xi"])
+            valid = o >= 0
+            mu_g = gst["mu"].cpu().numpy()[:, heads_kv]
+            assert np.array_equal(mu_g.view(np.uint64)[valid], ost["mu"].view(np.uint64)[valid]), c
+            np.testing.assert_array_equal(_np(gst["k"][:, heads_kv])[valid], ost["k"][valid])
+            np.testing.assert_array_equal(_np(gst["v"][:, heads_kv])[valid], ost["v"][valid])
         if c not in samples:
             continue
-        s_gpu = gpu.last_scores(0).cpu().numpy()
         out = out.cpu()
-        qc, kc, vc = q.cpu(), k.cpu(), v.cpu()
-        for g, heads in samples[c]:
+        qc = q.cpu()
+        for g in heads_kv:
+            heads = list(range(g * G, (g + 1) * G))
             outs, masses, order, n_c = _oracle_chunk(st, 0, g, qc, kc, vc, heads, cfg.ema_gamma,
                                                      cfg.rope_theta, scale)
             for h in heads:
                 err = np.abs(_np(out[0, :, h]) - outs[h]).max()
                 assert err <= 2e-2, (c, h, err)
-            if len(heads) == G:                                # full group: exact mass, max over heads
-                s_ref = reduce_heads(masses, G, "max")[0]
-                s_slots = np.concatenate([s_gpu[0, g, order], s_gpu[0, g, cfg.s_tot:cfg.s_tot + m]])
-                np.testing.assert_allclose(s_slots, s_ref, rtol=1e-3, atol=1e-30)
-                tot = 1 - cfg.ema_gamma ** m                   # each head's mass sums to 1 - gamma^m
-                assert tot * (1 - 1e-9) <= s_ref.sum() <= G * tot * (1 + 1e-9)
+            s_ref = reduce_heads(masses, G, "max")[0]
+            s_slots = np.concatenate([s_gpu[0, g, order], s_gpu[0, g, cfg.s_tot:cfg.s_tot + m]])
+            np.testing.assert_allclose(s_slots, s_ref, rtol=1e-3, atol=1e-30)
+            tot = 1 - cfg.ema_gamma ** m                   # each head's mass sums to 1 - gamma^m
+            assert tot * (1 - 1e-9) <= s_ref.sum() <= G * tot * (1 + 1e-9)
+    margins = rep.select_margins()
+    frac = float((margins <= 1e-3).mean())
+    print(f"cfg3 real run: {margins.size} selections on kv-heads {heads_kv}, min margin {margins.min():.3e}, "
+          f"fraction <= 1e-3: {frac:.2e}")
+    assert margins.size > 0 and margins.min() > 1e-3, (margins.min(), frac)
 
 
 def test_cfg4_decode_step_sampled_sequences_match_oracle():

@@ -291,3 +291,29 @@ def test_mean_head_reduction_keeps_the_sum_rule():
         outs.append(orc.prefill_stride(0, q1, k1, v1)[1])
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[0], outs[2])
+
+
+def test_q17_operand_rounding_moves_outputs_inside_the_bf16_tolerance():
+    """Reading Q17 (the rotated q, k the score products consume are bf16 in the bf16 configs) is
+    a choice the paper does not fix.  On the configs[1] input recipe the unrounded float64
+    oracle gives outputs within the north-star bf16 tolerance (2e-2) of the rounded one and the
+    same cascade contents (every selection margin >= 1e-3 either way); only the per-key masses
+    move by more than their 1e-3 parity tolerance, which is why the rounded reading is the one
+    the CUDA path is compared against."""
+    from paper_2406_17808_b200.synth import Synth, config_seed
+    B, Hq, Hk, d = 1, 8, 2, 128
+    mk = lambda r: CascadeOracle(OracleConfig(1, B, Hq, Hk, d, 64, 4096, 4, gamma=0.9999, rope_theta=5e5,
+                                              round_operands=r))
+    rounded, exact = mk("bf16"), mk("")
+    syn = Synth(B, Hq, Hk, d, config_seed(2))
+    f = lambda t: t.to(torch.float64).numpy()
+    worst_s = 0.0
+    for c in range(3):
+        q, k, v = syn.chunk(c * 1024, 1024)
+        oa, sa = rounded.prefill_stride(0, f(q), f(k), f(v))
+        ob, sb = exact.prefill_stride(0, f(q), f(k), f(v))
+        assert np.abs(oa - ob).max() < 2e-2
+        worst_s = max(worst_s, float(np.max(np.abs(sa - sb) / np.maximum(sb, 1e-30))))
+        np.testing.assert_array_equal(rounded.state(0)["origin"], exact.state(0)["origin"])
+    assert worst_s > 1e-3          # the masses DO depend on the reading
+    assert min(rounded.select_margins().min(), exact.select_margins().min()) > 1e-3
