@@ -34,7 +34,6 @@ struct LayerBufs {
   // per-call scratch (per layer so layers may run on different streams)
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   void* q_rot; void* k_rot; void* v_chunk;
-  float* dec_logits; float* dec_part_o; float* dec_part_ml;
   uint32_t* maint_ctl;      // [0] grid-barrier counter, then per-(b, g) 64-bit counts of rows
                             // actually rewritten (8-byte aligned)
   uint32_t maint_barrier;   // host copy of the barrier counter (wrapping)
@@ -74,8 +73,7 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 
 struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
-  size_t dec_logits, dec_part_o, dec_part_ml, maint_ctl;
-  int32_t dec_nsplit;
+  size_t maint_ctl;
   size_t per_layer;
   size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
   size_t total;
@@ -104,25 +102,12 @@ Sizes compute_sizes(const cascade_config& c) {
   z.q_rot = align_up(B * Hq * M * d * es);
   z.k_rot = align_up(B * Hk * (S + M) * d * es);
   z.v_chunk = align_up(B * Hk * M * d * es);
-  // decode scratch (bf16 only): logits per (slot, q-head of the group) and split partials
-  const size_t G = Hq / Hk;
-  z.dec_nsplit = 0;
-  z.dec_logits = z.dec_part_o = z.dec_part_ml = 0;
-  if (c.dtype == CASCADE_BF16) {
-    const size_t bgs = B * Hk;
-    // the most splits decode_attn_nsplit may pick (k_decode.cu): <= 64, >= 4 tiles per split
-    const size_t ns = std::max<size_t>(1, std::min<size_t>(64, ((S / 128 + 2 * N + 2) + 1 + 3) / 4));
-    z.dec_nsplit = (int32_t)ns;
-    z.dec_logits = align_up(bgs * (S + 1) * G * 4);
-    z.dec_part_o = align_up(bgs * ns * G * d * 4);
-    z.dec_part_ml = align_up(bgs * ns * G * 2 * 4);
-  }
   z.maint_ctl = align_up(8 + 8 * B * Hk);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk + z.dec_logits + z.dec_part_o + z.dec_part_ml + z.maint_ctl;
+                z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
-  z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(float2));
-  z.tab_lo = align_up(32 * (d / 2) * sizeof(float2));
+  z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(double2));
+  z.tab_lo = align_up(32 * (d / 2) * sizeof(double2));
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
@@ -143,8 +128,8 @@ struct cascade_handle {
   std::vector<cascade_mirror> mirrors;
   std::vector<int32_t> m_last;
   double2* rope_tab;     // [S_tot + max_stride][d/2] (cos, sin)(pos theta_i) in fp64
-  float2* tab_hi;
-  float2* tab_lo;
+  double2* tab_hi;       // [npos/32 + 1][d/2] (cos, sin)(32 a theta_i), fp64 (decode angle addition)
+  double2* tab_lo;       // [32][d/2] (cos, sin)(b theta_i), fp64
   void *stage_q, *stage_k, *stage_v, *stage_out;           // set 0 (aliases stage[0])
   struct Stage { void *q, *k, *v, *out; } stage[2];
   // pipelined host path (cascade_prefill_stride_host_async): copy streams and per-set events
@@ -326,15 +311,12 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.plan = reinterpret_cast<int32_t*>(take(sz.plan));
     L.resolved = reinterpret_cast<int32_t*>(take(sz.resolved));
     L.q_rot = take(sz.q_rot); L.k_rot = take(sz.k_rot); L.v_chunk = take(sz.v_chunk);
-    L.dec_logits = reinterpret_cast<float*>(take(sz.dec_logits));
-    L.dec_part_o = reinterpret_cast<float*>(take(sz.dec_part_o));
-    L.dec_part_ml = reinterpret_cast<float*>(take(sz.dec_part_ml));
     L.maint_ctl = reinterpret_cast<uint32_t*>(take(sz.maint_ctl));
     L.maint_barrier = 0;
   }
   h->rope_tab = reinterpret_cast<double2*>(take(sz.rope_tab));
-  h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
-  h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
+  h->tab_hi = reinterpret_cast<double2*>(take(sz.tab_hi));
+  h->tab_lo = reinterpret_cast<double2*>(take(sz.tab_lo));
   for (int i = 0; i < 2; ++i) {
     h->stage[i].q = take(sz.stage_q); h->stage[i].k = take(sz.stage_kv);
     h->stage[i].v = take(sz.stage_kv); h->stage[i].out = take(sz.stage_out);
@@ -399,16 +381,16 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
                           cudaMemcpyHostToDevice) == cudaSuccess;
     // angle-addition factors for decode: pe = 32 a + b, cos/sin(32 a theta_i) and cos/sin(b theta_i)
     const size_t nhi = npos / 32 + 1;
-    std::vector<float2> hi(nhi * half), lo(32 * half);
+    std::vector<double2> hi(nhi * half), lo(32 * half);
     for (int i = 0; i < half; ++i) {
       const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
       for (size_t a = 0; a < nhi; ++a)
-        hi[a * half + i] = make_float2((float)std::cos(32.0 * a * f), (float)std::sin(32.0 * a * f));
+        hi[a * half + i] = make_double2(std::cos((double)(32 * a) * f), std::sin((double)(32 * a) * f));
       for (int bb = 0; bb < 32; ++bb)
-        lo[bb * half + i] = make_float2((float)std::cos(bb * f), (float)std::sin(bb * f));
+        lo[bb * half + i] = make_double2(std::cos((double)bb * f), std::sin((double)bb * f));
     }
-    ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
-    ok = ok && cudaMemcpy(h->tab_lo, lo.data(), lo.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(double2), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->tab_lo, lo.data(), lo.size() * sizeof(double2), cudaMemcpyHostToDevice) == cudaSuccess;
   }
   ok = ok && cudaDeviceSynchronize() == cudaSuccess;
   if (!ok) { cascade_destroy(h); return CASCADE_ERR_CUDA; }
@@ -816,13 +798,10 @@ cascade_status cascade_host_wait(cascade_handle* h) {
 cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, const void* k,
                               const void* v, void* out, void* stream) {
   // q [B,Hq,d] is [B,1,Hq,d]: the m = 1 case of the strided step (Eq. 2).
-  // the fp32 toy, d = 64 and GQA groups other than 1 / 2 / 4 / 8 run the m = 1 case of the
-  // strided kernels; bf16 d = 128 with those groups (the Llama shapes) has the dedicated
-  // HBM-oriented decode kernels (instantiated per group size)
+  // bf16 with d = 128 (the Llama shapes, any GQA group <= 8) runs the fused cluster decode kernel
+  // (one launch); the fp32 toy and d = 64 run the m = 1 case of the strided kernels.
   if (h == nullptr || h->cfg.dtype != CASCADE_BF16 || h->cfg.head_dim != 128)
     return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  if (G != 1 && G != 2 && G != 4 && G != 8) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   cascade_status rc = check_call(h, layer, 1);
   if (rc != CASCADE_OK) return rc;
   if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
@@ -850,21 +829,23 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
   dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
   dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
-  dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
-  dp.logits = L.dec_logits; dp.part_o = L.dec_part_o; dp.part_ml = L.dec_part_ml;
-  dp.lse2 = L.lse;
+  dp.tab = h->rope_tab; dp.tab_hi64 = h->tab_hi; dp.tab_lo64 = h->tab_lo;
   dp.n_tiles = up.n_dec_tiles;
   dp.dec_tiles = up.dec_tiles;
-  dp.nsplit = std::min<int32_t>((int32_t)decode_attn_nsplit(dp), h->sz.dec_nsplit);
+  dp.nsplit = (int32_t)decode_nsplit(dp);
+  // a cache whose logits do not fit in TMEM even over 8 CTAs runs the m = 1 strided step (the
+  // plan just uploaded is scratch; the mirror has not advanced)
+  if (dp.nsplit == 0) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   const Plan& P = h->plan;
   {
     ProfScope ps(h, 4, st);
-    launch_decode(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin, (int32_t)P.phase_begin.size() - 1,
-                  static_cast<__nv_bfloat16*>(out), L.tm_kraw, L.tm_vs, st);
-    // algorithmic bytes: K, V (2 d bf16) + logits (4 G) + mu r/w + s per key
-    ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 4.0 * g.G + 16.0 + 4.0));
+    if (launch_decode(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin, (int32_t)P.phase_begin.size() - 1,
+                      static_cast<__nv_bfloat16*>(out), L.tm_kraw, L.tm_vs, st) != cudaSuccess)
+      return poison(h);
+    // algorithmic bytes: K, V (2 d bf16) + mu r/w + s per key
+    ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 16.0 + 4.0));
   }
-  h->launches += g.homogeneous ? 5 : 3;
+  h->launches += g.homogeneous ? 3 : 1;
   if (!launches_ok()) return poison(h);   // the update kernel folds mu and moves rows
   h->mirrors[layer] = next;
   h->m_last[layer] = 1;
@@ -924,6 +905,7 @@ cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
       cudaMemsetAsync(L.origin, 0xff, h->sz.origin, st) != cudaSuccess ||
+      cudaMemsetAsync(L.s, 0, h->sz.s, st) != cudaSuccess ||         // decode writes valid slots only
       cudaMemsetAsync(L.maint_ctl, 0, 4, st) != cudaSuccess)   // the barrier; the moved-row counts
                                                                // keep running
     return CASCADE_ERR_CUDA;

@@ -135,13 +135,13 @@ struct TcParams {
   double decay;                 // gamma^m
   int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
 };
-// single-token decode (k_decode.cu)
+// single-token decode (k_decode.cu): one fused cluster launch per step
 struct DecodeParams {
   int32_t B, Hq, Hkv, G, S_tot, alpha, N, c;
   int32_t sink_pre;
   int32_t counts[CASCADE_MAX_LEVELS], xi[CASCADE_MAX_LEVELS], base[CASCADE_MAX_LEVELS];
   int32_t n_keys;               // n_cached + 1 (the new token)
-  int32_t nsplit;
+  int32_t nsplit;               // CTAs per (b, g) = cluster size
   int32_t n_tiles;              // resident key tiles (the new token is one more)
   const int4* dec_tiles;        // (start slot, length, pe of key 0, unused) per tile
   int64_t t0;                   // stream index of the new token
@@ -150,8 +150,7 @@ struct DecodeParams {
   double decay;                 // gamma
   int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
   int32_t homogeneous;          // head policy: 0 independent, 1 homogeneous
-  int32_t update_stage;         // decode_update: 0 all; 1 scores only; 2 fold/select/move from s
-                                // (1 and 2 bracket the homogeneous-policy reduction; set by launch_decode)
+  int32_t update;               // fused kernel: 1 fold + insertion in-kernel; 0 s only (homogeneous)
   const __nv_bfloat16* q;       // [B][Hq][D]   pre-RoPE
   const __nv_bfloat16* k_new;   // [B][Hkv][D]
   const __nv_bfloat16* v_new;   // [B][Hkv][D]
@@ -161,17 +160,14 @@ struct DecodeParams {
   int64_t* origin;              // state
   float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
   const double2* tab;           // [npos][D/2] cos/sin(pe theta_i), fp64
-  const float2* tab_hi;         // [npos/32 + 1][D/2] cos/sin(32 a theta_i)
-  const float2* tab_lo;         // [32][D/2] cos/sin(b theta_i)
-  float* logits;                // [B*Hkv][S_tot + 1][G] log2-domain scaled logits
-  float* part_o;                // [B*Hkv][nsplit][G][D]
-  float* part_ml;               // [B*Hkv][nsplit][G][2]
-  float* lse2;                  // [B*Hq]
+  const double2* tab_hi64;      // [npos/32 + 1][D/2] cos/sin(32 a theta_i), fp64
+  const double2* tab_lo64;      // [32][D/2] cos/sin(b theta_i), fp64
 };
-size_t decode_attn_nsplit(const DecodeParams& p);
-void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                   int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
-                   cudaStream_t st);
+int decode_gm(int G);
+size_t decode_nsplit(const DecodeParams& p);   // 0: logits of the cache do not fit in TMEM
+cudaError_t launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
+                          int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
+                          cudaStream_t st);
 
 size_t attn_fwd_tc_smem(int d);
 

@@ -1,18 +1,34 @@
-// k_decode.cu -- single-token step (Eq. 2) + its cascade update, bf16.
+// k_decode.cu -- single-token step (Eq. 2) + its cascade update, bf16, ONE launch.
 //
 // Decode is HBM-bound (every cached K/V row is read once per step, ~4 flop/byte); the dot
 // products still run on the tensor cores (tcgen05, M = 128 keys x N = 16 query columns) so the
-// SIMT pipes are free for the per-key rotation and softmax:
-//   decode_attn     grid (b*Hkv, split): TMA-fed, warp-specialised (below); each CTA streams a
-//                   contiguous range of 128-slot key tiles, rotates every raw key in shared
-//                   memory to its rank pe, S^T = K_rot Q^T and O^T += V^T P^T in TMEM,
-//                   writes the log2-domain logits and the split's (max, sum, O).
-//   decode_combine  one CTA per (b, q-head): merges the splits -> O (bf16) and lse2.
-//   decode_update   one CTA per (b, g): exact mass s = w_0 * max_h exp2(logit_h - lse2_h)
-//                   (Alg. 3 with m = 1: w_0 = 1 - gamma; max over the group), EMA fold
-//                   mu <- gamma*mu + s for every resident, then Alg. 2's single
-//                   insertion: the (at most one) selection and the (at most N+1) row moves,
-//                   deepest sub-cache first.
+// SIMT pipes are free for the per-key rotation and softmax.
+//
+// decode_fused_kernel: grid (nsplit, B*Hkv), one thread-block CLUSTER of nsplit CTAs per (b, g).
+// Each CTA streams a contiguous range of the host's 128-slot key tiles (+ the new token's tile),
+// rotates every raw key to its rank pe in shared memory, S^T = K_rot Q^T and
+// O^T += V^T P^T in TMEM with an online softmax, and keeps every key's G log2-domain logits in
+// TMEM (a compact column region, GM columns per tile).  Then, inside the same kernel:
+//   1. cluster exchange (DSMEM) of each CTA's per-head (max, sum): every CTA knows the final
+//      LSE of the G heads;
+//   2. exact per-key mass s = w_0 * max_h exp2(logit_h - lse2_h) (Alg. 3 with m = 1: w_0 =
+//      1 - gamma; max over the group; mean / median ablations) from the logits still in
+//      TMEM -- no logits round trip through HBM -- written to s and folded into mu
+//      (mu <- gamma * mu + s, IEEE double, never an FMA);
+//   3. cluster rank 0 merges the CTAs' scaled partial O (DSMEM) into the bf16 output;
+//   4. cluster rank 0 applies Alg. 2's single insertion: the (at most one) selection
+//      on the folded mu (strict '>') and the (at most N+1) row moves, deepest sub-cache
+//      first -- after a cluster barrier, so every CTA's fold is visible and every CTA's K/V
+//      reads are done.
+// The homogeneous head policy needs a reduction over the kv-heads of a sequence, i.e.
+// across clusters: the fused kernel then only writes s, and decode_update_kernel folds, selects
+// and moves after head_homogenize_kernel.
+//
+// Rotation precision (reading Q17): the key operand is the bf16 rounding of R(pe) k with the
+// rotation in float64 -- cos/sin((32 a + b) theta_i) by angle addition from two float64 tables
+// (a-rows staged per tile, b-rows resident), products and sums in double, rounded double ->
+// float -> bf16 -- so the operand is the oracle's bf16 value (its float64 rotation rounded the
+// same way) up to a ~1e-16 relative difference in cos/sin.
 #include "common.cuh"
 
 #include <cmath>
@@ -21,86 +37,90 @@
 namespace cascade {
 
 namespace {
-
-
+constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
+constexpr int kLoRows = 32;                                  // pe = 32 a + b
+constexpr int kRowBytes = 64 * 16;                           // 64 rotate-half pairs x double2
+constexpr int kLoStride = kRowBytes + 16;                    // padded bytes per b-row (bank spread)
+constexpr int kKStages = 3, kVStages = 2;
+constexpr int kKStageBytes = 32768 + kHiRows * kRowBytes;    // 37888: K tile + a-rows, 1 KB multiple
+constexpr int kVStageBytes = 32768;
+constexpr uint32_t kColLg = 64;                              // compact logits: GM columns per tile
+constexpr uint32_t kTmemCols = 512;
 }  // namespace
 
-// Tensor-core decode attention (D = 128), TMA-fed and warp-specialised.  One CTA per
-// (b*Hkv, split); the keys are the host's resident tile list (128-slot runs of one sub-cache,
-// contiguous in memory) plus a 1-key tile for the new token.
-//   warp 0     producer: TMA of the raw K tile (SWIZZLE_128B) + the cos/sin rows of the tile's
-//              32-position blocks (bulk copies) into a 3-stage K ring, freed by QK^T
-//   warp 3     producer: TMA of the V tile into a 3-stage V ring, freed by PV (split from the K
-//              ring so K runs ahead of V: 0.924 -> 0.890 ms per configs[3] step)
+size_t decode_fused_smem(int GM) {
+  return (size_t)kKStages * kKStageBytes + (size_t)kVStages * kVStageBytes + 4096 + 4096 +
+         (size_t)kLoRows * kLoStride + (size_t)GM * 128 * 4 + 4 * 8 * 4 + 40 * 4 + 64 + 24 * 8 + 1024;
+}
+int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
+
+// Tensor-core decode, warp roles (512 threads):
+//   warp 0     producer: TMA of the raw K tile (SWIZZLE_128B) + the float64 cos/sin rows of the
+//              tile's 32-position blocks (bulk copies) into a 3-stage K ring, freed by QK^T
+//   warp 3     producer: TMA of the V tile into a 2-stage V ring, freed by PV
 //   warp 1     MMA: S^T[128 keys x 16] = K_rot Q^T (two S^T buffers, so QK(j+1) runs during
 //              softmax(j)), then O^T[128 d x 16] += V^T P^T
 //   warp 2     TMEM allocator
-//   warps 4-7  softmax: thread t = key t: logits, online softmax per head, P^T
+//   warps 4-7  softmax: thread t = key t: logits (kept in TMEM), online softmax per head, P^T
 //   warps 8-15 two rotation warpgroups (half of the rotate-half pairs each): rotate every raw
-//              key IN PLACE to its rank pe (cos/sin of (32a + b) theta by angle addition:
-//              a-rows from the stage, b-rows resident), round to bf16 (reading Q17); they run
-//              up to a full ring ahead of the softmax.
+//              key IN PLACE to its rank pe; they run up to a full ring ahead of the softmax.
+// After the tiles, warps 4-15 compute the masses and the fold; rank 0's softmax warps merge O
+// and its warp 0 applies the insertion.
 // Tile descriptor (int4, host): start slot, length, pe of key 0 (pe of key j = pe0 + j: the host
 // splits a tile where a full ring wraps past its oldest slot).
-namespace {
-constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
-constexpr int kLoRows = 32;                                  // pe = 32 a + b
-constexpr int kLoStride = 64 * 8 + 8;                        // padded bytes per b-row (bank spread)
-constexpr int kDecStages = 3;
-}
-
-template <int G>
-__global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_constant__ CUtensorMap tm_k,
-                                                             const __grid_constant__ CUtensorMap tm_v,
-                                                             DecodeParams p) {
+template <int GM>
+__global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
+                                                              const __grid_constant__ CUtensorMap tm_v,
+                                                              DecodeParams p, PlanDev pl, int32_t n_sel,
+                                                              const int32_t* __restrict__ phase_begin,
+                                                              int32_t n_phase, __nv_bfloat16* __restrict__ out) {
   constexpr int D = 128, HALF = 64;
-  // K and V have separate rings: a K stage (32 KB + the tile's a-rows, padded to 1 KB for the next
-  // stage's SWIZZLE_128B alignment) is free once QK^T has read it, a V stage (32 KB) once PV has
-  constexpr int kKStageBytes = (32768 + kHiRows * 512 + 1023) / 1024 * 1024;
-  constexpr int kVStageBytes = 32768;
-  // All shared memory is dynamic (no static variables, so the window starts 1024-B aligned and
-  // three stages fit): stages | Q | P | cos/sin(b theta) rows | small scalars and barriers.
-  extern __shared__ __align__(1024) uint8_t dsm[];
-  uint8_t* sK = dsm;                                        // kDecStages x [K | a-rows]
-  uint8_t* sV = sK + kDecStages * kKStageBytes;             // kDecStages x V
-  uint8_t* sQ = sV + kDecStages * kVStageBytes;             // [16 rows x 128 d] SW128 (2 x 2 KB)
+  extern __shared__ __align__(1024) uint8_t dsm_raw[];
+  uint8_t* dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
+  uint8_t* sK = dsm;                                        // kKStages x [K | a-rows]
+  uint8_t* sV = sK + kKStages * kKStageBytes;               // kVStages x V
+  uint8_t* sQ = sV + kVStages * kVStageBytes;               // [16 rows x 128 d] SW128 (2 x 2 KB)
   uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
-  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i)
-  float (*sRed)[G] = reinterpret_cast<float (*)[G]>(sLo + kLoRows * kLoStride);   // [4][G]
-  float* sCorr = reinterpret_cast<float*>(sRed + 4);
-  int* sRescale = reinterpret_cast<int*>(sCorr + G);
-  uint32_t* sTmemP = reinterpret_cast<uint32_t*>(sRescale + 1);
-  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sTmemP + 1) + 7) & ~uintptr_t(7));
+  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i), fp64
+  float* sO = reinterpret_cast<float*>(sLo + kLoRows * kLoStride);   // [GM][128] scaled partial O
+  float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sO + GM * 128);  // [4][8]
+  float* sML = reinterpret_cast<float*>(sRed + 4);          // [0, 8) max, [8, 16) sum, [16, 24) lse2
+  float* sCorr = sML + 24;                                  // [8]
+  int* sRescale = reinterpret_cast<int*>(sCorr + 8);
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(sRescale + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sTmem + 1) + 7) & ~uintptr_t(7));
   uint64_t* kfull = bars + 0;       // [3]
   uint64_t* kempty = bars + 3;      // [3]
   uint64_t* rot_full = bars + 6;    // [3 stages][2 rotation warpgroups]
   uint64_t* s_full = bars + 12;     // [2] per S^T buffer
   uint64_t* p_full = bars + 14;     // [2] per S^T buffer
   uint64_t* pv_done = bars + 16;
-  uint64_t* vfull = bars + 17;      // [3]
-  uint64_t* vempty = bars + 20;     // [3]
+  uint64_t* vfull = bars + 17;      // [2]
+  uint64_t* vempty = bars + 19;     // [2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bg = blockIdx.x, split = blockIdx.y;
+  const int split = blockIdx.x, bg = blockIdx.y;
+  const uint32_t crank = tc::cluster_ctarank();            // == split (cluster = the splits of bg)
+  const int ns = gridDim.x;
+  const int G = p.G;
   const int b = bg / p.Hkv, g = bg - b * p.Hkv;
   const int n_tiles = p.n_tiles + 1;                         // + the new-token tile
-  const int per = (n_tiles + p.nsplit - 1) / p.nsplit;
+  const int per = (n_tiles + ns - 1) / ns;
   const int tbeg = split * per, tend = min(n_tiles, tbeg + per);
   const int nt = max(0, tend - tbeg);
 
   if (tid == 0) {
-    for (int i = 0; i < kDecStages; ++i) {
-      tc::mbar_init(kfull + i, 1); tc::mbar_init(kempty + i, 1);
-      tc::mbar_init(vfull + i, 1); tc::mbar_init(vempty + i, 1);
-    }
-    for (int i = 0; i < 2 * kDecStages; ++i) tc::mbar_init(rot_full + i, 4);
+    for (int i = 0; i < kKStages; ++i) { tc::mbar_init(kfull + i, 1); tc::mbar_init(kempty + i, 1); }
+    for (int i = 0; i < kVStages; ++i) { tc::mbar_init(vfull + i, 1); tc::mbar_init(vempty + i, 1); }
+    for (int i = 0; i < 2 * kKStages; ++i) tc::mbar_init(rot_full + i, 4);
     for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
     tc::mbar_init(pv_done, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_v); }
-  if (warp == 2) tc::tmem_alloc<64>(sTmemP);
-  // group queries rotated to pe = n_cached, bf16 (rows >= G zero); cos/sin(b theta) rows
+  if (warp == 2) tc::tmem_alloc<kTmemCols>(sTmem);
+  // group queries rotated to pe = n_cached (float64 rotation, Q17), bf16 (rows >= G zero);
+  // cos/sin(b theta) rows
   for (int o = tid; o < 16 * HALF; o += blockDim.x) {
     const int h = o / HALF, i = o - h * HALF;
     float r1 = 0.f, r2 = 0.f;
@@ -116,13 +136,13 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
     *reinterpret_cast<__nv_bfloat16*>(sQ + 2048 + off) = __float2bfloat16_rn(r2);
   }
   for (int o = tid; o < kLoRows * HALF; o += blockDim.x)
-    *reinterpret_cast<float2*>(sLo + (o / HALF) * kLoStride + (o % HALF) * 8) = p.tab_lo[o];
+    *reinterpret_cast<double2*>(sLo + (o / HALF) * kLoStride + (o % HALF) * 16) = p.tab_lo64[o];
   for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = *sTmemP, tO = tmem + 16;          // S^T buffers at columns 0 and 32
+  const uint32_t tmem = *sTmem, tO = tmem + 16;            // S^T buffers at columns 0 and 32
 
   // per-tile geometry (same on every warp): start slot, length, pe of key 0
   auto tile_info = [&](int ti, int& start, int& len, int& pe0) {
@@ -137,27 +157,27 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
   if (warp == 0) {
     if (tc::elect_one()) {
       for (int j = 0; j < nt; ++j) {              // K tiles + a-rows
-        const int s = j % kDecStages;
-        if (j >= kDecStages) tc::mbar_wait(kempty + s, ((j / kDecStages) - 1) & 1);
+        const int s = j % kKStages;
+        if (j >= kKStages) tc::mbar_wait(kempty + s, ((j / kKStages) - 1) & 1);
         int start, len, pe0;
         tile_info(tbeg + j, start, len, pe0);
         uint8_t* st = sK + s * kKStageBytes;
-        // a-rows of the tile's pe range [pe0, pe0 + len)
         const int a0 = pe0 >> 5, nA = ((pe0 + len - 1) >> 5) - a0 + 1;
-        const uint32_t bytes = (start < p.S_tot ? 32768u : 0u) + (uint32_t)nA * 512u;
+        const uint32_t bytes = (start < p.S_tot ? 32768u : 0u) + (uint32_t)nA * kRowBytes;
         tc::mbar_expect_tx(kfull + s, bytes);
         if (start < p.S_tot) {
           const int row = (int)((long long)bg * p.S_tot + start);
           for (int kb = 0; kb < 2; ++kb) tc::tma_load_2d(st + kb * 16384, &tm_k, kfull + s, kb * 64, row);
         }
-        for (int r = 0; r < nA; ++r) tc::bulk_load(st + 32768 + r * 512, p.tab_hi + (long long)(a0 + r) * HALF, 512, kfull + s);
+        for (int r = 0; r < nA; ++r)
+          tc::bulk_load(st + 32768 + r * kRowBytes, p.tab_hi64 + (long long)(a0 + r) * HALF, kRowBytes, kfull + s);
       }
     }
   } else if (warp == 3) {
     if (tc::elect_one()) {
       for (int j = 0; j < nt; ++j) {              // V tiles (the new token's V is written by the rotation warps)
-        const int s = j % kDecStages;
-        if (j >= kDecStages) tc::mbar_wait(vempty + s, ((j / kDecStages) - 1) & 1);
+        const int s = j % kVStages;
+        if (j >= kVStages) tc::mbar_wait(vempty + s, ((j / kVStages) - 1) & 1);
         int start, len, pe0;
         tile_info(tbeg + j, start, len, pe0);
         uint8_t* st = sV + s * kVStageBytes;
@@ -176,10 +196,10 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, 16, 0, 1);
       const uint32_t aQ = tc::smem_u32(sQ), aP = tc::smem_u32(sP);
       auto qk = [&](int j) {
-        const int s = j % kDecStages;
+        const int s = j % kKStages;
         const uint32_t st = tc::smem_u32(sK + s * kKStageBytes);
-        tc::mbar_wait(rot_full + 2 * s, (j / kDecStages) & 1);       // both rotated halves in place
-        tc::mbar_wait(rot_full + 2 * s + 1, (j / kDecStages) & 1);
+        tc::mbar_wait(rot_full + 2 * s, (j / kKStages) & 1);       // both rotated halves in place
+        tc::mbar_wait(rot_full + 2 * s + 1, (j / kKStages) & 1);
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -193,10 +213,10 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       if (nt > 0) qk(0);
       for (int j = 0; j < nt; ++j) {
         if (j + 1 < nt) qk(j + 1);                          // overlaps softmax(j)
-        const int s = j % kDecStages;
+        const int s = j % kVStages;
         const uint32_t st = tc::smem_u32(sV + s * kVStageBytes);
         tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);       // P^T written (and O^T rescaled)
-        tc::mbar_wait(vfull + s, (j / kDecStages) & 1);
+        tc::mbar_wait(vfull + s, (j / kVStages) & 1);
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -213,20 +233,20 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
     const int t = (tid - 256) & 127;                         // key row of the tile
     const int rwg = (tid - 256) >> 7;                        // chunks [4 rwg, 4 rwg + 4)
     for (int j = 0; j < nt; ++j) {
-      const int s = j % kDecStages;
+      const int s = j % kKStages;
       uint8_t* st = sK + s * kKStageBytes;
       int start, len, pe0;
       tile_info(tbeg + j, start, len, pe0);
       const bool valid = t < len;
       const int pe = pe0 + t;
-      tc::mbar_wait(kfull + s, (j / kDecStages) & 1);
+      tc::mbar_wait(kfull + s, (j / kKStages) & 1);
       if (start < p.S_tot) {
         // ---- rotate row t in place: pairs (i, i + 64) live at the same swizzled offset of the
-        //      two 64-column blocks ----
+        //      two 64-column blocks; cos/sin((32a + b) theta_i) by angle addition in double ----
         const int hr = (pe >> 5) - (pe0 >> 5);
-        const float2* hi = reinterpret_cast<const float2*>(st + 32768 + (valid ? hr : 0) * 512);
-        const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
-#pragma unroll 2
+        const double2* hi = reinterpret_cast<const double2*>(st + 32768 + (valid ? hr : 0) * kRowBytes);
+        const double2* lo = reinterpret_cast<const double2*>(sLo + (pe & 31) * kLoStride);
+#pragma unroll 1
         for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = t * 128 + ((c ^ (t & 7)) << 4);
           uint4* pa = reinterpret_cast<uint4*>(st + off);
@@ -240,13 +260,13 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int i = c * 8 + 2 * e2 + u;
-              const float2 h2 = hi[i], l2 = lo[i];
-              const float cs = h2.x * l2.x - h2.y * l2.y;  // cos((32a + b) theta_i)
-              const float sn = h2.y * l2.x + h2.x * l2.y;  // sin((32a + b) theta_i)
-              const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
-              const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
-              r[u] = x1 * cs - x2 * sn;
-              r[2 + u] = x2 * cs + x1 * sn;
+              const double2 h2 = hi[i], l2 = lo[i];
+              const double cs = fma(h2.x, l2.x, -(h2.y * l2.y));    // cos((32a + b) theta_i)
+              const double sn = fma(h2.y, l2.x, h2.x * l2.y);       // sin((32a + b) theta_i)
+              const double x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
+              const double x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
+              r[u] = __double2float_rn(fma(x1, cs, -(x2 * sn)));
+              r[2 + u] = __double2float_rn(fma(x2, cs, x1 * sn));
             }
             oa[e2] = tc::pack_bf16(r[0], r[1]);
             ob[e2] = tc::pack_bf16(r[2], r[3]);
@@ -257,8 +277,9 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       } else {
         // ---- the new token: key row 0 from the input, rotated to n_cached; rows >= 1 zero;
         //      its V row goes to the V stage once that is free ----
-        tc::mbar_wait(vfull + s, (j / kDecStages) & 1);
-        uint8_t* sv = sV + s * kVStageBytes;
+        const int sv_i = j % kVStages;
+        tc::mbar_wait(vfull + sv_i, (j / kVStages) & 1);
+        uint8_t* sv = sV + sv_i * kVStageBytes;
         const int off_base = t * 128;
         for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = off_base + ((c ^ (t & 7)) << 4);
@@ -303,29 +324,29 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
     const int t = tid - 128;                                 // key = TMEM lane
     const int w4 = warp & 3;
     const uint32_t lane_off = (uint32_t)(w4 * 32) << 16;
-    float m_run[G], l_part[G];
+    float m_run[GM], l_part[GM];
 #pragma unroll
-    for (int h = 0; h < G; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
+    for (int h = 0; h < GM; ++h) { m_run[h] = -INFINITY; l_part[h] = 0.f; }
     for (int j = 0; j < nt; ++j) {
       int start, len, pe0;
       tile_info(tbeg + j, start, len, pe0);
       const bool valid = t < len;
-      // ---- logits, block max per head, P^T ----
+      // ---- logits (kept in TMEM for the mass), block max per head, P^T ----
       tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc::tc_fence_after();
       float sv[16];
       tc::tmem_ld16(tmem + (j & 1) * 32 + lane_off, sv);
       tc::tmem_wait_ld();
-      float lg[G];
+      float lg[GM];
+      uint32_t lgb[GM];
 #pragma unroll
-      for (int h = 0; h < G; ++h) lg[h] = valid ? sv[h] * p.scale_log2 : -INFINITY;
-      if (valid) {
-        float* lp = p.logits + ((long long)bg * (p.S_tot + 1) + start + t) * G;
-#pragma unroll
-        for (int h = 0; h < G; ++h) lp[h] = lg[h];
+      for (int h = 0; h < GM; ++h) {
+        lg[h] = (valid && h < G) ? sv[h] * p.scale_log2 : -INFINITY;
+        lgb[h] = __float_as_uint(lg[h]);
       }
+      tc::tmem_st_n<GM>(tmem + lane_off + kColLg + (uint32_t)(GM * j), lgb);
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int h = 0; h < GM; ++h) {
         float v = lg[h];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -335,12 +356,12 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       if (t == 0) {
         int any = 0;
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
+        for (int h = 0; h < GM; ++h) {
           const float mt = fmaxf(fmaxf(sRed[0][h], sRed[1][h]), fmaxf(sRed[2][h], sRed[3][h]));
           const float mn = fmaxf(m_run[h], mt);
-          const float cr = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+          const float cr = (m_run[h] == -INFINITY) ? 0.f : exp2f(m_run[h] - mn);
           sCorr[h] = cr;
-          any |= (j > 0 && cr != 1.f);
+          any |= (j > 0 && m_run[h] != -INFINITY && cr != 1.f);
           sRed[0][h] = mn;
         }
         *sRescale = any;
@@ -349,11 +370,11 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       tc::named_bar_sync(1, 128);
       tc::tc_fence_after();
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int h = 0; h < GM; ++h) {
         const float mn = sRed[0][h];
         const float cr = sCorr[h];
         m_run[h] = mn;
-        const float pv = valid ? exp2f(lg[h] - mn) : 0.f;
+        const float pv = (valid && h < G) ? exp2f(lg[h] - mn) : 0.f;
         l_part[h] = l_part[h] * cr + pv;
         const int blk = t >> 6, kc = t & 63;
         *reinterpret_cast<__nv_bfloat16*>(sP + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
@@ -364,7 +385,7 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
         tc::tmem_ld16(tO + lane_off, ov);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int h = 0; h < G; ++h) ov[h] *= sCorr[h];
+        for (int h = 0; h < GM; ++h) ov[h] *= sCorr[h];
         tc::tmem_st16(tO + lane_off, reinterpret_cast<const uint32_t*>(ov));
         tc::tmem_wait_st();
       }
@@ -374,146 +395,189 @@ __global__ void __launch_bounds__(512, 1) decode_attn_kernel(const __grid_consta
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
     }
-    // ---- split results ----
-    {
+    // ---- this CTA's per-head (max, sum) ----
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
+    for (int h = 0; h < GM; ++h) {
       float v = l_part[h];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) sRed[w4][h] = v;
     }
-    if (nt > 0) tc::mbar_wait(pv_done, (nt - 1) & 1);
-    tc::tc_fence_after();
+    if (nt > 0) tc::mbar_wait(pv_done, (nt - 1) & 1);      // O^T holds every tile
+    tc::tmem_wait_st();
     tc::named_bar_sync(1, 128);
-    const long long pbase = ((long long)bg * p.nsplit + split) * G;
-    if (t < G) {
-      p.part_ml[(pbase + t) * 2] = m_run[t];
-      p.part_ml[(pbase + t) * 2 + 1] = sRed[0][t] + sRed[1][t] + sRed[2][t] + sRed[3][t];
-    }
-    float ov[16];
-    tc::tmem_ld16(tO + lane_off, ov);
-    tc::tmem_wait_ld();
-#pragma unroll
-    for (int h = 0; h < G; ++h) p.part_o[(pbase + h) * D + t] = nt > 0 ? ov[h] : 0.f;
+    if (t < GM) {
+      sML[t] = m_run[t];
+      sML[8 + t] = sRed[0][t] + sRed[1][t] + sRed[2][t] + sRed[3][t];
     }
   }
+  // ======== cluster exchange #1: every CTA's (max, sum) per head ========
   tc::tc_fence_before();
   __syncthreads();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  if (tid < GM) {                                            // final log2-domain LSE of head tid
+    float M = -INFINITY;
+    for (int r = 0; r < ns; ++r) M = fmaxf(M, tc::ld_cluster_f32(sML + tid, (uint32_t)r));
+    float L = 0.f;
+    for (int r = 0; r < ns; ++r) {
+      const float mr = tc::ld_cluster_f32(sML + tid, (uint32_t)r);
+      if (mr != -INFINITY) L += tc::ld_cluster_f32(sML + 8 + tid, (uint32_t)r) * exp2f(mr - M);
+    }
+    sML[16 + tid] = M + log2f(L);
+    sCorr[tid] = (sML[tid] == -INFINITY) ? 0.f : exp2f(sML[tid] - M) / L;   // this CTA's O weight
+  }
+  __syncthreads();
+  if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;                          // 0..2: three warpgroups share the tiles
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int t = (warp & 3) * 32 + lane;                    // key (or d) = TMEM lane
+    if (wg == 0) {                                           // scaled partial O^T -> sO (own smem)
+      float ov[16];
+      tc::tmem_ld16(tO + lane_off, ov);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int h = 0; h < GM; ++h) sO[h * 128 + t] = ov[h] * sCorr[h];
+    }
+    // ---- exact per-key mass (Alg. 3, m = 1) + EMA fold, from the logits in TMEM ----
+    float lse[GM];
+#pragma unroll
+    for (int h = 0; h < GM; ++h) lse[h] = sML[16 + h];
+    double* mu = p.mu + (long long)bg * p.S_tot;
+    float* s_out = p.s + (long long)bg * (p.S_tot + 1);
+    // kU tiles per round: every TMEM load and mu load of the round is issued before the first
+    // use, so the tail streams instead of paying one load round trip per tile
+    constexpr int kU = 4;
+    for (int j0 = wg; j0 < nt; j0 += 3 * kU) {
+      uint32_t lgb[kU][GM];
+      double m0[kU];
+      int xs[kU];
+      bool vk[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = j0 + 3 * u;
+        int start = 0, len = 0, pe0 = 0;
+        if (j < nt) {
+          tile_info(tbeg + j, start, len, pe0);
+          tc::tmem_ld_n<GM>(tmem + lane_off + kColLg + (uint32_t)(GM * j), lgb[u]);
+        }
+        vk[u] = j < nt && t < len;
+        xs[u] = start + t;
+        m0[u] = (vk[u] && xs[u] < p.S_tot && p.update) ? mu[xs[u]] : 0.0;
+      }
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!vk[u]) continue;
+        float best = 0.f;
+        if (p.head_reduce == 0) {
+#pragma unroll
+          for (int h = 0; h < GM; ++h)
+            if (h < G) best = fmaxf(best, exp2f(__uint_as_float(lgb[u][h]) - lse[h]));
+        } else {                                             // mean / median ablations
+          float hv[GM];
+#pragma unroll
+          for (int h = 0; h < GM; ++h) hv[h] = h < G ? exp2f(__uint_as_float(lgb[u][h]) - lse[h]) : 0.f;
+          best = group_reduce_ablation(hv, G, p.head_reduce);
+        }
+        const float sv = p.w0 * best;
+        s_out[xs[u]] = sv;
+        if (xs[u] < p.S_tot && p.update) mu[xs[u]] = __dadd_rn(__dmul_rn(p.decay, m0[u]), (double)sv);
+      }
+    }
+  }
+  // ======== cluster exchange #2: every fold and every s visible; partial O staged ========
+  __threadfence();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  if (crank == 0) {
+    if (warp >= 4 && warp < 8) {                             // O = sum over the cluster's CTAs
+      const int d = tid - 128;
+      for (int h = 0; h < G; ++h) {
+        float o = 0.f;
+        for (int r = 0; r < ns; ++r) o += tc::ld_cluster_f32(sO + h * 128 + d, (uint32_t)r);
+        out[((long long)b * p.Hq + g * G + h) * D + d] = __float2bfloat16_rn(o);
+      }
+    } else if (warp == 0 && p.update) {
+      // ---- Alg. 2's single insertion: selections (depth order), then moves deepest first ----
+      double* mu = p.mu + (long long)bg * p.S_tot;
+      const float* s_out = p.s + (long long)bg * (p.S_tot + 1);
+      int32_t* res = pl.resolved + (long long)bg * pl.sel_cap;
+      if (lane == 0) {
+        for (int jj = 0; jj < n_sel; ++jj) {
+          const int k = pl.sel_order[jj];
+          int32_t cand = pl.sel[3 * k + 1], inc = pl.sel[3 * k + 2];
+          cand = cand >= 0 ? cand : res[-cand - 1];
+          inc = inc >= 0 ? inc : res[-inc - 1];
+          const double mc = cand < p.S_tot ? mu[cand] : (double)s_out[cand];
+          const double mi = inc < p.S_tot ? mu[inc] : (double)s_out[inc];
+          res[k] = mc > mi ? cand : inc;                    // strict '>'
+        }
+      }
+      __syncwarp();
+      for (int ph = 0; ph < n_phase; ++ph) {
+        for (int e = phase_begin[ph]; e < phase_begin[ph + 1]; ++e) {
+          const int32_t dst = pl.mov[2 * e];
+          int32_t src = pl.mov[2 * e + 1];
+          src = src >= 0 ? src : res[-src - 1];
+          if (src == dst) continue;
+          const __nv_bfloat16 *ks, *vs;
+          double mu_new;
+          int64_t org;
+          if (src < p.S_tot) {
+            ks = p.k_raw_mut + ((long long)bg * p.S_tot + src) * D;
+            vs = p.v_mut + ((long long)bg * p.S_tot + src) * D;
+            mu_new = mu[src];
+            org = p.origin[(long long)bg * p.S_tot + src];
+          } else {
+            ks = p.k_new + (long long)bg * D;
+            vs = p.v_new + (long long)bg * D;
+            mu_new = (double)s_out[src];
+            org = p.t0;
+          }
+          __nv_bfloat16* kd = p.k_raw_mut + ((long long)bg * p.S_tot + dst) * D;
+          __nv_bfloat16* vd = p.v_mut + ((long long)bg * p.S_tot + dst) * D;
+          constexpr int NV = D * 2 / 16;
+          const uint4 kv = reinterpret_cast<const uint4*>(ks)[lane & (NV - 1)];
+          const uint4 vv = reinterpret_cast<const uint4*>(vs)[lane & (NV - 1)];
+          __syncwarp();                                    // every lane read before any write
+          if (lane < NV) reinterpret_cast<uint4*>(kd)[lane] = kv;
+          else reinterpret_cast<uint4*>(vd)[lane - NV] = vv;
+          if (lane == 0) { mu[dst] = mu_new; p.origin[(long long)bg * p.S_tot + dst] = org; }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  // ======== #3: peers keep their shared memory until rank 0 has read it ========
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();
   if (warp == 2) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<64>(tmem);
+    tc::tmem_dealloc<kTmemCols>(tmem);
   }
 }
 
-template <int D>
-__global__ void decode_combine_kernel(DecodeParams p, __nv_bfloat16* __restrict__ out) {
-  const int bh = blockIdx.x, d = threadIdx.x;
-  const int b = bh / p.Hq, h = bh - b * p.Hq;
-  const int g = h / p.G, j = h - g * p.G;
-  const long long bg = (long long)b * p.Hkv + g;
-  float M = -INFINITY;
-  for (int s = 0; s < p.nsplit; ++s) M = fmaxf(M, p.part_ml[((bg * p.nsplit + s) * p.G + j) * 2]);
-  float L = 0.f, o = 0.f;
-  for (int s = 0; s < p.nsplit; ++s) {
-    const long long base = (bg * p.nsplit + s) * p.G + j;
-    const float ms = p.part_ml[base * 2];
-    if (ms == -INFINITY) continue;
-    const float f = exp2f(ms - M);
-    L += p.part_ml[base * 2 + 1] * f;
-    o += p.part_o[base * D + d] * f;
-  }
-  out[(long long)bh * D + d] = __float2bfloat16_rn(o / L);
-  if (d == 0) p.lse2[bh] = M + log2f(L);
-}
-
-// One CTA per (b, g).  Plan (uploaded by the host): the m = 1 schedule of Alg. 2.
+// Stage 2 of the homogeneous head policy, one CTA per (b, g): s already holds the
+// per-sequence reduction (head_homogenize_kernel); fold it into mu, then the selections and
+// moves of the single insertion.
 template <int D>
 __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, PlanDev pl, int32_t n_sel,
                                                             const int32_t* __restrict__ phase_begin,
                                                             int32_t n_phase) {
   const int bg = blockIdx.x, tid = threadIdx.x;
-  const int b = bg / p.Hkv, g = bg - b * p.Hkv;
-  __shared__ float sl[16];
-  if (tid < p.G) sl[tid] = p.lse2[(long long)b * p.Hq + g * p.G + tid];
-  __syncthreads();
   double* mu = p.mu + (long long)bg * p.S_tot;
   float* s_out = p.s + (long long)bg * (p.S_tot + 1);
-  const float* lg = p.logits + (long long)bg * (p.S_tot + 1) * p.G;
-  // 1. exact mass + fold for every valid slot, run by run (sinks, C_1 .. C_N); the new token's
-  //    mass lands at S_tot.  Empty slots keep s = 0 (zeroed when the layer was reset / init).
-  const float4* lg4 = reinterpret_cast<const float4*>(lg);
-  if (p.G == 4 && p.head_reduce == 0 && p.update_stage == 0) {
-    // the common case (GQA 4:1, max): kU slots per thread in flight -- every logit / mu load of
-    // the batch is issued before the first use, so the pass streams at HBM rate rather than at
-    // one load round trip per slot
-    constexpr int kU = 4;
-    for (int run = 0; run <= p.N; ++run) {
-      const int beg = run == 0 ? 0 : p.alpha + (run - 1) * p.c;
-      const int len = run == 0 ? p.sink_pre : p.counts[run - 1];
-      const int cap = run == 0 ? p.alpha : p.c;
-      for (int o0 = tid; o0 < cap; o0 += kU * blockDim.x) {
-        float4 l[kU];
-        double m[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int o = o0 + u * blockDim.x;
-          if (o < len) { l[u] = __ldcs(lg4 + beg + o); m[u] = mu[beg + o]; }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int o = o0 + u * blockDim.x, x = beg + o;
-          if (o >= cap) continue;
-          if (o >= len) { s_out[x] = 0.f; continue; }
-          const float best = fmaxf(fmaxf(exp2f(l[u].x - sl[0]), exp2f(l[u].y - sl[1])),
-                                   fmaxf(exp2f(l[u].z - sl[2]), exp2f(l[u].w - sl[3])));
-          const float sv = p.w0 * best;
-          s_out[x] = sv;
-          mu[x] = __dadd_rn(__dmul_rn(p.decay, m[u]), (double)sv);
-        }
-      }
-    }
-  } else
   for (int run = 0; run <= p.N; ++run) {
     const int beg = run == 0 ? 0 : p.alpha + (run - 1) * p.c;
     const int len = run == 0 ? p.sink_pre : p.counts[run - 1];
-    const int cap = run == 0 ? p.alpha : p.c;
-    for (int o = tid; o < cap; o += blockDim.x) {
-      const int x = beg + o;
-      if (o >= len) { s_out[x] = 0.f; continue; }
-      if (p.update_stage == 2) {                           // s already reduced (homogeneous)
-        mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)s_out[x]);
-        continue;
-      }
-      float best = 0.f;
-      if (p.head_reduce) {                                 // mean / median ablations
-        float hv[kMaxMedianGroup];
-        for (int h = 0; h < p.G; ++h) hv[h] = exp2f(lg[(long long)x * p.G + h] - sl[h]);
-        best = group_reduce_ablation(hv, p.G, p.head_reduce);
-      } else if (p.G == 4) {
-        const float4 l = lg4[x];
-        best = fmaxf(fmaxf(exp2f(l.x - sl[0]), exp2f(l.y - sl[1])), fmaxf(exp2f(l.z - sl[2]), exp2f(l.w - sl[3])));
-      } else {
-        for (int h = 0; h < p.G; ++h) best = fmaxf(best, exp2f(lg[(long long)x * p.G + h] - sl[h]));
-      }
-      const float sv = p.w0 * best;
-      s_out[x] = sv;
-      if (p.update_stage == 0) mu[x] = __dadd_rn(__dmul_rn(p.decay, mu[x]), (double)sv);
-    }
+    for (int o = tid; o < len; o += blockDim.x)
+      mu[beg + o] = __dadd_rn(__dmul_rn(p.decay, mu[beg + o]), (double)s_out[beg + o]);
   }
-  if (tid == 0 && p.update_stage != 2) {
-    float best = 0.f, hv[kMaxMedianGroup];
-    for (int h = 0; h < p.G; ++h) {
-      const float e = exp2f(lg[(long long)p.S_tot * p.G + h] - sl[h]);
-      if (h < kMaxMedianGroup) hv[h] = e;           // G <= 32 whenever an ablation is on
-      best = fmaxf(best, e);
-    }
-    if (p.head_reduce) best = group_reduce_ablation(hv, p.G, p.head_reduce);
-    s_out[p.S_tot] = p.w0 * best;
-  }
-  if (p.update_stage == 1) return;                         // scores only (homogeneous, stage 1)
   __syncthreads();
-  // 2. selections (depth order), 3. moves deepest sub-cache first -- one warp, sequential
   if (tid < 32) {
     int32_t* res = pl.resolved + (long long)bg * pl.sel_cap;
     if (tid == 0) {
@@ -551,8 +615,11 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
         __nv_bfloat16* kd = p.k_raw_mut + ((long long)bg * p.S_tot + dst) * D;
         __nv_bfloat16* vd = p.v_mut + ((long long)bg * p.S_tot + dst) * D;
         constexpr int NV = D * 2 / 16;
-        if (tid < NV) reinterpret_cast<uint4*>(kd)[tid] = reinterpret_cast<const uint4*>(ks)[tid];
-        else if (tid < 2 * NV) reinterpret_cast<uint4*>(vd)[tid - NV] = reinterpret_cast<const uint4*>(vs)[tid - NV];
+        const uint4 kv = reinterpret_cast<const uint4*>(ks)[tid & (NV - 1)];
+        const uint4 vv = reinterpret_cast<const uint4*>(vs)[tid & (NV - 1)];
+        __syncwarp();
+        if (tid < NV) reinterpret_cast<uint4*>(kd)[tid] = kv;
+        else reinterpret_cast<uint4*>(vd)[tid - NV] = vv;
         if (tid == 0) { mu[dst] = mu_new; p.origin[(long long)bg * p.S_tot + dst] = org; }
         __syncwarp();
       }
@@ -560,51 +627,67 @@ __global__ void __launch_bounds__(256) decode_update_kernel(DecodeParams p, Plan
   }
 }
 
-size_t decode_attn_nsplit(const DecodeParams& p) {
-  // splits per (b, g): minimise (waves of 1-CTA-per-SM CTAs) x (tiles per CTA + ~4 tiles of
-  // per-CTA pipeline fill / combine overhead); >= 4 tiles per split.  Measured at B = 64,
-  // Hkv = 8, 129 tiles (scripts/dbench.py): 1 / 2 / 3 / 4 / 5 / 6 / 8 / 12 splits ->
-  // 1.010 / 0.922 / 0.968 / 0.954 / 0.985 / 0.984 / 1.014 / 1.066 ms per step; the model picks 2.
+int decode_gm(int G) { return G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : 8; }
+
+size_t decode_nsplit(const DecodeParams& p) {
+  // splits per (b, g) = cluster size: minimise (waves of 1-CTA-per-SM CTAs) x (tiles per CTA +
+  // ~4 tiles of per-CTA pipeline fill / epilogue), subject to every tile's logits fitting in TMEM;
+  // clusters of 2 tile the 148 SMs exactly, clusters of 4 strand 16 of them (B300_MICROARCH.md)
+  const int GM = decode_gm(p.G);
+  const int tiles = p.n_tiles + 1, cap = decode_fused_max_tiles(GM);
   const int bgs = p.B * p.Hkv;
-  const int cap = std::max(1, std::min(64, (p.n_tiles + 1 + 3) / 4));
-  int best = 1;
+  int best = 0;
   double best_cost = 1e300;
-  for (int ns = 1; ns <= cap; ++ns) {
-    const double waves = std::ceil((double)bgs * ns / 148.0);
-    const double cost = waves * ((double)(p.n_tiles + 1) / ns + 4.0);
+  for (int ns : {1, 2, 4, 8}) {
+    const int per = (tiles + ns - 1) / ns;
+    if (per > cap) continue;
+    const double sms = ns <= 2 ? 148.0 : ns == 4 ? 132.0 : 128.0;
+    const double cost = std::ceil((double)bgs * ns / sms) * (per + 4.0);
     if (cost < best_cost) { best_cost = cost; best = ns; }
   }
-  return (size_t)best;
+  return (size_t)best;            // 0: the cache is too large for the in-TMEM logits
 }
 
-template <int G>
-void launch_attn(const DecodeParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
-  const size_t smem = kDecStages * ((32768 + kHiRows * 512 + 1023) / 1024 * 1024 + 32768) + 4096 + 4096 +
-                      kLoRows * kLoStride + 4 * G * 4 + G * 4 + 8 + 8 + 23 * 8;
-  cudaFuncSetAttribute(decode_attn_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  decode_attn_kernel<G><<<dim3(p.B * p.Hkv, p.nsplit), 512, smem, st>>>(tk, tv, p);
+template <int GM>
+cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
+                         int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
+                         cudaStream_t st) {
+  const size_t smem = decode_fused_smem(GM);
+  auto kern = decode_fused_kernel<GM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.nsplit, p.B * p.Hkv);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.nsplit;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tk, tv, p, pl, n_sel, phase_begin_dev, n_phase, out);
 }
 
-void launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                   int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
-                   cudaStream_t st) {
-  if (p.G == 4) launch_attn<4>(p, tk, tv, st);
-  else if (p.G == 1) launch_attn<1>(p, tk, tv, st);
-  else if (p.G == 2) launch_attn<2>(p, tk, tv, st);
-  else launch_attn<8>(p, tk, tv, st);
-  decode_combine_kernel<128><<<p.B * p.Hq, 128, 0, st>>>(p, out);
-  if (!p.homogeneous) {
-    decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
-    return;
-  }
-  // homogeneous head policy: every kv-head's s, then one reduction per sequence, then
-  // the fold / selections / moves from the reduced s
-  DecodeParams q = p;
-  q.update_stage = 1;
-  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(q, pl, n_sel, phase_begin_dev, n_phase);
+cudaError_t launch_decode(const DecodeParams& p_in, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
+                          int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
+                          cudaStream_t st) {
+  DecodeParams p = p_in;
+  p.update = p.homogeneous ? 0 : 1;
+  const int GM = decode_gm(p.G);
+  cudaError_t e;
+  if (GM == 1) e = launch_fused<1>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  else if (GM == 2) e = launch_fused<2>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  else if (GM == 4) e = launch_fused<4>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  else e = launch_fused<8>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  if (e != cudaSuccess || !p.homogeneous) return e;
+  // homogeneous head policy: one reduction per sequence over its kv-heads' s, then the
+  // fold / selections / moves from the reduced s
   launch_head_homogenize(p.B, p.Hkv, p.S_tot + 1, p.head_reduce, p.s, st);
-  q.update_stage = 2;
-  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(q, pl, n_sel, phase_begin_dev, n_phase);
+  decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
+  return cudaGetLastError();
 }
 
 }  // namespace cascade
