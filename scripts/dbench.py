@@ -29,5 +29,5 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / (steps - 3)
 n_c = cas.state(0)["n_cached"]
-byt = B * 8 * (n_c + 1) * (4 * 128 + 36)
+byt = B * 8 * (n_c + 1) * (4 * 128 + 20)   # K, V + mu r/w + s per key
 print(f"B={B} n_cached={n_c}: {ms:.3f} ms/step, {B / ms * 1e3:,.0f} tok/s, {byt / ms / 1e6:,.0f} GB/s algorithmic")
