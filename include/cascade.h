@@ -205,6 +205,44 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
 cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out,
                              void* stream);
 
+/* ---- split step: attention, then (after an optional cross-device reduction of
+ * the per-key mass) the cache update --------------------------------------- */
+
+/* The two halves of one Alg. 1 step, for head policies whose per-key
+ * mass must be reduced across devices: the homogeneous policy under
+ * kv-head sharding needs s reduced over the kv-heads of every rank.
+ *   cascade_attend   RoPE by rank, attention (out written, as cascade_prefill_stride /
+ *                    cascade_decode for m = 1) and the exact per-key mass s of every
+ *                    local kv-head (reduced over its GQA group; homogeneous policy: also
+ *                    over the local kv-heads, so every local kv-head holds the same row).
+ *                    Independent heads: the EMA fold of the residents may already be
+ *                    applied (it needs no cross-device data).  No token is inserted and
+ *                    the mirror does not advance.
+ *   cascade_score_buffer  device pointer to the layer's s, [B][Hkv][row_len] fp32,
+ *                    row_len = S_tot + m (flat slot space); the caller may reduce it in
+ *                    place on `stream` (e.g. NCCL all_reduce MAX across the ranks).
+ *   cascade_commit   the EMA fold (unless applied) and Alg. 2's insertion of the m
+ *                    tokens from the (reduced) s; k, v must be the buffers passed to
+ *                    cascade_attend, still valid; advances the mirror.
+ * Between an attend and its commit every other call on that layer returns
+ * CASCADE_ERR_ORDER.  cascade_prefill_stride == attend + commit. */
+cascade_status cascade_attend(cascade_handle* h, int32_t layer, const void* q, const void* k,
+                              const void* v, int32_t m, void* out, void* stream);
+cascade_status cascade_score_buffer(cascade_handle* h, int32_t layer, float** s, int32_t* row_len);
+cascade_status cascade_commit(cascade_handle* h, int32_t layer, const void* k, const void* v,
+                              void* stream);
+
+/* Checkpoint restore: overwrite one layer's cascade with `src`, a
+ * state with the same geometry (num_cascades, sub_cache_size, sink_size, slots_total,
+ * head_dim, dtype, batch, num_kv_heads; else CONFIG), e.g. one exported by cascade_state
+ * of another handle and copied out.  src->k_raw / v [B][Hkv][S_tot][d] (dtype), mu fp64
+ * and origin int64 [B][Hkv][S_tot] may be device or (pinned) host memory; they are copied
+ * on `stream` (cudaMemcpyDefault).  The mirror must be reachable by Alg. 2 (sinks fill
+ * first; a sub-cache that is not full holds slots [0, count) with xi = count,
+ * P:160; t >= residents) else INVALID_ARG.  pe is derived, not read. */
+cascade_status cascade_load_state(cascade_handle* h, int32_t layer, const cascade_state_view* src,
+                                  void* stream);
+
 /* ---- test hooks -------------------------------------------------------- */
 
 /* Score injection: fold the given per-key mass and insert the m tokens, with

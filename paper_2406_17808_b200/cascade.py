@@ -87,6 +87,10 @@ def lib():
             "cascade_reset": (i32, [vp, i32, vp]),
             "cascade_profile_enable": (i32, [vp, i32]),
             "cascade_profile_read": (i32, [vp, vp, vp, vp]),
+            "cascade_attend": (i32, [vp, i32, vp, vp, vp, i32, vp, vp]),
+            "cascade_score_buffer": (i32, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(i32)]),
+            "cascade_commit": (i32, [vp, i32, vp, vp, vp]),
+            "cascade_load_state": (i32, [vp, i32, ctypes.POINTER(_StateView), vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -102,7 +106,8 @@ EXPORTED = ["cascade_status_string", "cascade_validate_config", "cascade_workspa
             "cascade_decode", "cascade_state",
             "cascade_update_with_scores", "cascade_last_scores", "cascade_mirror_advance",
             "cascade_launch_count", "cascade_reset", "cascade_profile_enable",
-            "cascade_profile_read"]
+            "cascade_profile_read", "cascade_attend", "cascade_score_buffer", "cascade_commit",
+            "cascade_load_state"]
 
 
 @dataclass
@@ -284,6 +289,48 @@ class Cascade:
         rc = lib().cascade_decode(self._h, layer, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _stream(stream))
         _check(rc, "cascade_decode")
         return out
+
+    # ---- split step (cross-device reduction of s between attention and update) ----
+    def attend(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+               out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Attention + per-key mass of one step (cascade_attend); q/k/v shaped as for
+        prefill_stride ([B, m, H, d]; m = 1 runs the fused decode kernel)."""
+        m = q.shape[1]
+        if out is None:
+            out = torch.empty_like(q)
+        self._check_io((q, k, v, out), self._chunk_shapes(m))
+        rc = lib().cascade_attend(self._h, layer, _ptr(q), _ptr(k), _ptr(v), m, _ptr(out), _stream(stream))
+        _check(rc, "cascade_attend")
+        return out
+
+    def score_buffer(self, layer: int) -> torch.Tensor:
+        """The pending step's per-key mass [B, Hkv, S_tot + m] (a view of library memory: reduce
+        it in place, e.g. dist.all_reduce(..., MAX), before commit)."""
+        ptr, n = ctypes.c_void_p(), ctypes.c_int32(0)
+        _check(lib().cascade_score_buffer(self._h, layer, ctypes.byref(ptr), ctypes.byref(n)),
+               "cascade_score_buffer")
+        shape = (self.cfg.batch, self.cfg.num_kv_heads, n.value)
+        return torch.as_tensor(_DevArray(ptr.value, shape, "<f4"), device=self.device)
+
+    def commit(self, layer: int, k: torch.Tensor, v: torch.Tensor, stream=None) -> None:
+        _check(lib().cascade_commit(self._h, layer, _ptr(k), _ptr(v), _stream(stream)), "cascade_commit")
+
+    def load_state(self, layer: int, st: dict, stream=None) -> None:
+        """Restores a layer from a state dict as returned by state() (checkpoint restore)."""
+        sv = _StateView()
+        mr = sv.mirror
+        mr.t, mr.sink_count = st["t"], st["sink_count"]
+        for i, (cnt, xi) in enumerate(zip(st["counts"], st["xi"])):
+            mr.counts[i], mr.xi[i] = cnt, xi
+        sv.num_cascades, sv.sub_cache_size, sv.sink_size = self.cfg.num_cascades, self.cfg.c, self.cfg.sink_size
+        sv.slots_total, sv.head_dim = self.cfg.s_tot, self.cfg.head_dim
+        sv.dtype, sv.batch, sv.num_kv_heads = (BF16 if self.cfg.dtype == "bf16" else F32), self.cfg.batch, \
+            self.cfg.num_kv_heads
+        keep = [st[n].contiguous() for n in ("k", "v", "mu", "origin")]
+        sv.k_raw, sv.v, sv.mu, sv.origin = (t.data_ptr() for t in keep)
+        rc = lib().cascade_load_state(self._h, layer, ctypes.byref(sv), _stream(stream))
+        (stream or torch.cuda.current_stream(self.device)).synchronize()   # `keep` is freed on return
+        _check(rc, "cascade_load_state")
 
     # ---- test hooks / export ---------------------------------------------------
     def update_with_scores(self, layer: int, k: torch.Tensor, v: torch.Tensor, s: torch.Tensor,

@@ -119,6 +119,39 @@ Sizes compute_sizes(const cascade_config& c) {
 
 }  // namespace
 
+namespace {
+// Builds the plan for the layer's next m tokens, uploads it (plus the EMA row weights) and
+// advances the mirror.  Returns the device plan view and phase/depth offsets via h->plan.
+struct Upload {
+  PlanDev pd;
+  const float* w;        // [m] EMA row weights (1 - gamma) gamma^(m-1-r)
+  const float* log2w;    // [m] their log2 (-inf when w == 0)
+  const int2* tiles;     // resident key tiles (start slot, valid length)
+  int32_t n_tiles;
+  const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
+  const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
+  int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
+  const int4* maint_staged;    // moves that read a resident slot (MaintItems::staged)
+  int32_t n_maint_staged;
+  const int4* maint_chunk;     // moves that read no resident slot (MaintItems::chunk)
+  int32_t n_maint_chunk;
+};
+
+// An attend (cascade_attend) whose commit is outstanding, per layer.  The host Plan is shared by
+// the layers, so the pending one keeps a copy.
+struct Pending {
+  bool active = false;
+  bool decode = false;       // fused decode attend (commit = decode_update_kernel)
+  bool folded = false;       // prefill: pass 2 already folded mu (independent heads, tcgen05 path)
+  int32_t m = 0;
+  Geometry g{};
+  Upload up{};
+  cascade_mirror next{};
+  Plan plan;
+  DecodeParams dp{};
+};
+}  // namespace
+
 struct cascade_handle {
   cascade_config cfg;
   int device;
@@ -127,6 +160,7 @@ struct cascade_handle {
   std::vector<LayerBufs> layers;
   std::vector<cascade_mirror> mirrors;
   std::vector<int32_t> m_last;
+  std::vector<Pending> pending;   // per layer: an attend awaiting its commit
   double2* rope_tab;     // [S_tot + max_stride][d/2] (cos, sin)(pos theta_i) in fp64
   double2* tab_hi;       // [npos/32 + 1][d/2] (cos, sin)(32 a theta_i), fp64 (decode angle addition)
   double2* tab_lo;       // [32][d/2] (cos, sin)(b theta_i), fp64
@@ -325,6 +359,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->stage_v = h->stage[0].v; h->stage_out = h->stage[0].out;
   h->mirrors.assign(cfg->num_layers, cascade_mirror{});
   h->m_last.assign(cfg->num_layers, 0);
+  h->pending.assign(cfg->num_layers, Pending{});
 
   bool ok = true;
   ok = ok && cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) == cudaSuccess &&
@@ -422,23 +457,6 @@ Geometry make_geometry(const cascade_handle* h, const cascade_mirror& mr, int32_
   g.homogeneous = c.head_policy == 1;
   return g;
 }
-
-// Builds the plan for the layer's next m tokens, uploads it (plus the EMA row weights) and
-// advances the mirror.  Returns the device plan view and phase/depth offsets via h->plan.
-struct Upload {
-  PlanDev pd;
-  const float* w;        // [m] EMA row weights (1 - gamma) gamma^(m-1-r)
-  const float* log2w;    // [m] their log2 (-inf when w == 0)
-  const int2* tiles;     // resident key tiles (start slot, valid length)
-  int32_t n_tiles;
-  const int32_t* phase_begin;  // plan phase offsets (N + 2 phases + end)
-  const int4* dec_tiles;       // resident tiles with rank geometry (start, len, pe0, unused)
-  int32_t n_dec_tiles;         // > n_tiles when full rings wrap inside a 128-slot tile
-  const int4* maint_staged;    // moves that read a resident slot (MaintItems::staged)
-  int32_t n_maint_staged;
-  const int4* maint_chunk;     // moves that read no resident slot (MaintItems::chunk)
-  int32_t n_maint_chunk;
-};
 
 cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStream_t st,
                            Upload* up, cascade_mirror* next) {
@@ -586,12 +604,11 @@ cascade_status poison(cascade_handle* h) {
 // then the cooperative move launch.  Every launch here mutates state; returns false on a launch
 // error (the caller poisons the handle).
 template <typename T>
-bool launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up,
+bool launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, const Upload& up, const Plan& P,
                         const T* k, const T* v, const float* s, bool folded, cudaStream_t st) {
-  const Plan& P = h->plan;
   const PlanDev& pd = up.pd;
   ProfScope ps(h, 3, st);
-  if (!folded) {          // the score producer did not fold mu (injection, SIMT path)
+  if (!folded) {          // the score producer did not fold mu (injection, SIMT path, homogeneous)
     launch_ema_fold(g, L.mu, s, st);
     ++h->launches;
   }
@@ -629,9 +646,14 @@ bool launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
   return true;
 }
 
+// The attention half of one Alg. 1 step (rows a2-a4): RoPE by rank, pass 1 (out, LSE), pass 2
+// (exact per-key mass s, reduced over each GQA group; independent heads on the tcgen05 path also
+// fold it into mu in pass 2's epilogue) and, homogeneous heads, the reduction of s over the
+// sequence's local kv-heads.  Nothing of the cascade is inserted; *pd receives what the commit
+// needs.  fold_ok = false keeps mu untouched (the split API with homogeneous heads).
 template <typename T>
-cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const T* k, const T* v,
-                            int32_t m, T* out, cudaStream_t st) {
+cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, const T* k, const T* v,
+                              int32_t m, T* out, cudaStream_t st, Pending* pd) {
   LayerBufs& L = h->layers[layer];
   const Geometry g = make_geometry(h, h->mirrors[layer], m);
   Upload up;
@@ -675,7 +697,7 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
   }
   h->launches += 2;
   if (!launches_ok()) return CASCADE_ERR_CUDA;   // nothing of the cascade state has changed yet
-  // from here on every launch mutates the cascade state (pass 2 folds mu in its epilogue)
+  // from here on a launch may mutate the cascade state (pass 2 folds mu in its epilogue)
   if constexpr (kTc) {
     if (h->cfg.ema_gamma != 1.0) {
       ProfScope ps(h, 2, st);
@@ -696,11 +718,110 @@ cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const 
     launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
     ++h->launches;
   }
-  if (!launches_ok()) return poison(h);
-  if (!launch_maintenance<T>(h, g, L, up, k, v, L.s, /*folded=*/kTc && !g.homogeneous, st) || !launches_ok())
+  const bool folded = kTc && !g.homogeneous;
+  if (!launches_ok()) return folded ? poison(h) : CASCADE_ERR_CUDA;
+  pd->active = true; pd->decode = false; pd->folded = folded; pd->m = m;
+  pd->g = g; pd->up = up; pd->next = next; pd->plan = h->plan;
+  return CASCADE_OK;
+}
+
+// The insertion half (rows a5-a7): fold (unless pass 2 did) + Alg. 2 maintenance; commits the mirror.
+template <typename T>
+cascade_status commit_prefill(cascade_handle* h, int32_t layer, const T* k, const T* v, cudaStream_t st,
+                              Pending& pd) {
+  LayerBufs& L = h->layers[layer];
+  pd.active = false;
+  if (!launch_maintenance<T>(h, pd.g, L, pd.up, pd.plan, k, v, L.s, pd.folded, st) || !launches_ok())
     return poison(h);
-  h->mirrors[layer] = next;   // commit the mirror
-  h->m_last[layer] = m;
+  h->mirrors[layer] = pd.next;   // commit the mirror
+  h->m_last[layer] = pd.m;
+  return CASCADE_OK;
+}
+
+template <typename T>
+cascade_status prefill_impl(cascade_handle* h, int32_t layer, const T* q, const T* k, const T* v,
+                            int32_t m, T* out, cudaStream_t st) {
+  Pending& pd = h->pending[layer];
+  const cascade_status rc = attend_prefill<T>(h, layer, q, k, v, m, out, st, &pd);
+  if (rc != CASCADE_OK) return rc;
+  return commit_prefill<T>(h, layer, k, v, st, pd);
+}
+
+// Decode attention + mass on the fused cluster kernel.  commit_inline: the independent head
+// policy lets the kernel fold and insert itself (one launch); otherwise it writes s only and
+// (homogeneous heads) the local kv-heads' s are reduced, leaving the fold / selection / moves to
+// commit_decode.  Returns CASCADE_ERR_UNSUPPORTED (nothing launched, mirror untouched) when the
+// cache's logits do not fit in TMEM.
+cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat16* q, const __nv_bfloat16* k,
+                             const __nv_bfloat16* v, __nv_bfloat16* out, cudaStream_t st, bool commit_inline,
+                             Pending* pd) {
+  LayerBufs& L = h->layers[layer];
+  const Geometry g = make_geometry(h, h->mirrors[layer], 1);
+  Upload up;
+  cascade_mirror next;
+  cascade_status rc = upload_plan(h, layer, 1, st, &up, &next);
+  if (rc != CASCADE_OK) return rc;
+  DecodeParams dp{};
+  dp.B = g.B; dp.Hq = g.Hq; dp.Hkv = g.Hkv; dp.G = g.G; dp.S_tot = g.S_tot; dp.alpha = g.alpha;
+  dp.N = g.N; dp.c = g.c; dp.sink_pre = g.sink_pre;
+  for (int i = 0; i < g.N; ++i) { dp.counts[i] = g.counts_pre[i]; dp.xi[i] = g.xi_pre[i]; dp.base[i] = g.base_pre[i]; }
+  dp.n_keys = g.n_cached + 1;
+  dp.t0 = g.t0;
+  dp.scale_log2 = g.scale_log2;
+  dp.w0 = (float)((1.0 - h->cfg.ema_gamma) * gamma_pow(h->cfg.ema_gamma, 0));
+  dp.decay = g.decay;
+  dp.head_reduce = g.head_reduce;
+  dp.homogeneous = g.homogeneous;
+  dp.update = commit_inline && !g.homogeneous ? 1 : 0;
+  dp.q = q; dp.k_new = k; dp.v_new = v;
+  dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
+  dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
+  dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
+  dp.tab = h->rope_tab; dp.tab_hi64 = h->tab_hi; dp.tab_lo64 = h->tab_lo;
+  dp.n_tiles = up.n_dec_tiles;
+  dp.dec_tiles = up.dec_tiles;
+  dp.nsplit = (int32_t)decode_nsplit(dp);
+  if (dp.nsplit == 0) return CASCADE_ERR_UNSUPPORTED;   // the uploaded plan is scratch
+  // the kernel writes s of valid slots only: after a step of another layout (prefill rows
+  // S_tot + m, injection, reset) the empty slots' entries must read 0 (cascade_last_scores)
+  if (h->m_last[layer] != 1 &&
+      cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + 1) * sizeof(float), st) != cudaSuccess)
+    return CASCADE_ERR_CUDA;
+  const Plan& P = h->plan;
+  {
+    ProfScope ps(h, 4, st);
+    const bool ok = launch_decode_fused(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin,
+                                        (int32_t)P.phase_begin.size() - 1, out, L.tm_kraw, L.tm_vs,
+                                        st) == cudaSuccess;
+    ++h->launches;
+    if (ok && g.homogeneous) {          // one s per sequence over the local kv-heads
+      launch_head_homogenize(g.B, g.Hkv, g.S_tot + 1, g.head_reduce, L.s, st);
+      ++h->launches;
+    }
+    if (!ok || !launches_ok()) return dp.update ? poison(h) : CASCADE_ERR_CUDA;
+    // algorithmic bytes: K, V (2 d bf16) + mu r/w + s per key
+    ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + (dp.update ? 20.0 : 4.0)));
+  }
+  pd->active = true; pd->decode = true; pd->folded = false; pd->m = 1;
+  pd->g = g; pd->up = up; pd->next = next; pd->plan = h->plan; pd->dp = dp;
+  return CASCADE_OK;
+}
+
+cascade_status commit_decode(cascade_handle* h, int32_t layer, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                             cudaStream_t st, Pending& pd) {
+  pd.active = false;
+  if (!pd.dp.update) {                  // fold + selection + moves from s
+    DecodeParams dp = pd.dp;
+    dp.k_new = k; dp.v_new = v;
+    ProfScope ps(h, 3, st);
+    const bool ok = launch_decode_commit(dp, pd.up.pd, (int32_t)pd.plan.sel_order.size(), pd.up.phase_begin,
+                                         (int32_t)pd.plan.phase_begin.size() - 1, st) == cudaSuccess;
+    ++h->launches;
+    if (!ok || !launches_ok()) return poison(h);
+    ps.finish((double)pd.g.B * pd.g.Hkv * pd.g.n_cached * 20.0);
+  }
+  h->mirrors[layer] = pd.next;
+  h->m_last[layer] = 1;
   return CASCADE_OK;
 }
 
@@ -709,8 +830,13 @@ cascade_status check_call(cascade_handle* h, int32_t layer, int32_t m) {
   if (h->poisoned) return CASCADE_ERR_POISONED;
   (void)cudaGetLastError();   // a stale non-sticky error of an earlier runtime call is not ours
   if (layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (h->pending[layer].active) return CASCADE_ERR_ORDER;   // cascade_commit first
   if (m < 1 || m > h->cfg.max_stride) return CASCADE_ERR_SHAPE;
   return CASCADE_OK;
+}
+
+bool fused_decode_eligible(const cascade_handle* h) {
+  return h->cfg.dtype == CASCADE_BF16 && h->cfg.head_dim == 128;
 }
 
 }  // namespace
@@ -799,57 +925,66 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
                               const void* v, void* out, void* stream) {
   // q [B,Hq,d] is [B,1,Hq,d]: the m = 1 case of the strided step (Eq. 2).
   // bf16 with d = 128 (the Llama shapes, any GQA group <= 8) runs the fused cluster decode kernel
-  // (one launch); the fp32 toy and d = 64 run the m = 1 case of the strided kernels.
-  if (h == nullptr || h->cfg.dtype != CASCADE_BF16 || h->cfg.head_dim != 128)
-    return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
+  // (one launch); the fp32 toy, d = 64 and caches whose logits do not fit in TMEM run the m = 1
+  // case of the strided kernels.
+  if (h == nullptr || !fused_decode_eligible(h)) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   cascade_status rc = check_call(h, layer, 1);
   if (rc != CASCADE_OK) return rc;
   if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  LayerBufs& L = h->layers[layer];
-  const Geometry g = make_geometry(h, h->mirrors[layer], 1);
-  Upload up;
-  cascade_mirror next;
-  rc = upload_plan(h, layer, 1, st, &up, &next);
+  const auto* kb = static_cast<const __nv_bfloat16*>(k);
+  const auto* vb = static_cast<const __nv_bfloat16*>(v);
+  Pending& pd = h->pending[layer];
+  rc = attend_decode(h, layer, static_cast<const __nv_bfloat16*>(q), kb, vb, static_cast<__nv_bfloat16*>(out),
+                     st, /*commit_inline=*/true, &pd);
+  if (rc == CASCADE_ERR_UNSUPPORTED) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   if (rc != CASCADE_OK) return rc;
-  DecodeParams dp{};
-  dp.B = g.B; dp.Hq = g.Hq; dp.Hkv = g.Hkv; dp.G = g.G; dp.S_tot = g.S_tot; dp.alpha = g.alpha;
-  dp.N = g.N; dp.c = g.c; dp.sink_pre = g.sink_pre;
-  for (int i = 0; i < g.N; ++i) { dp.counts[i] = g.counts_pre[i]; dp.xi[i] = g.xi_pre[i]; dp.base[i] = g.base_pre[i]; }
-  dp.n_keys = g.n_cached + 1;
-  dp.t0 = g.t0;
-  dp.scale_log2 = g.scale_log2;
-  dp.w0 = (float)((1.0 - h->cfg.ema_gamma) * gamma_pow(h->cfg.ema_gamma, 0));
-  dp.decay = g.decay;
-  dp.head_reduce = g.head_reduce;
-  dp.homogeneous = g.homogeneous;
-  dp.q = static_cast<const __nv_bfloat16*>(q);
-  dp.k_new = static_cast<const __nv_bfloat16*>(k);
-  dp.v_new = static_cast<const __nv_bfloat16*>(v);
-  dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
-  dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
-  dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
-  dp.tab = h->rope_tab; dp.tab_hi64 = h->tab_hi; dp.tab_lo64 = h->tab_lo;
-  dp.n_tiles = up.n_dec_tiles;
-  dp.dec_tiles = up.dec_tiles;
-  dp.nsplit = (int32_t)decode_nsplit(dp);
-  // a cache whose logits do not fit in TMEM even over 8 CTAs runs the m = 1 strided step (the
-  // plan just uploaded is scratch; the mirror has not advanced)
-  if (dp.nsplit == 0) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
-  const Plan& P = h->plan;
-  {
-    ProfScope ps(h, 4, st);
-    if (launch_decode(dp, up.pd, (int32_t)P.sel_order.size(), up.phase_begin, (int32_t)P.phase_begin.size() - 1,
-                      static_cast<__nv_bfloat16*>(out), L.tm_kraw, L.tm_vs, st) != cudaSuccess)
-      return poison(h);
-    // algorithmic bytes: K, V (2 d bf16) + mu r/w + s per key
-    ps.finish((double)g.B * g.Hkv * (g.n_cached + 1) * (4.0 * g.d + 16.0 + 4.0));
+  return commit_decode(h, layer, kb, vb, st, pd);
+}
+
+cascade_status cascade_attend(cascade_handle* h, int32_t layer, const void* q, const void* k, const void* v,
+                              int32_t m, void* out, void* stream) {
+  cascade_status rc = check_call(h, layer, m);
+  if (rc != CASCADE_OK) return rc;
+  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Pending& pd = h->pending[layer];
+  if (m == 1 && fused_decode_eligible(h)) {
+    rc = attend_decode(h, layer, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+                       static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(out), st,
+                       /*commit_inline=*/false, &pd);
+    if (rc != CASCADE_ERR_UNSUPPORTED) return rc;
   }
-  h->launches += g.homogeneous ? 3 : 1;
-  if (!launches_ok()) return poison(h);   // the update kernel folds mu and moves rows
-  h->mirrors[layer] = next;
-  h->m_last[layer] = 1;
+  if (h->cfg.dtype == CASCADE_BF16)
+    return attend_prefill<__nv_bfloat16>(h, layer, static_cast<const __nv_bfloat16*>(q),
+                                         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v),
+                                         m, static_cast<__nv_bfloat16*>(out), st, &pd);
+  return attend_prefill<float>(h, layer, static_cast<const float*>(q), static_cast<const float*>(k),
+                               static_cast<const float*>(v), m, static_cast<float*>(out), st, &pd);
+}
+
+cascade_status cascade_score_buffer(cascade_handle* h, int32_t layer, float** s, int32_t* row_len) {
+  if (!h || !s || !row_len || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  const Pending& pd = h->pending[layer];
+  if (!pd.active) return CASCADE_ERR_ORDER;
+  *s = h->layers[layer].s;
+  *row_len = h->S_tot + pd.m;
   return CASCADE_OK;
+}
+
+cascade_status cascade_commit(cascade_handle* h, int32_t layer, const void* k, const void* v, void* stream) {
+  if (!h || !k || !v || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (h->poisoned) return CASCADE_ERR_POISONED;
+  (void)cudaGetLastError();
+  Pending& pd = h->pending[layer];
+  if (!pd.active) return CASCADE_ERR_ORDER;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pd.decode)
+    return commit_decode(h, layer, static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), st, pd);
+  if (h->cfg.dtype == CASCADE_BF16)
+    return commit_prefill<__nv_bfloat16>(h, layer, static_cast<const __nv_bfloat16*>(k),
+                                         static_cast<const __nv_bfloat16*>(v), st, pd);
+  return commit_prefill<float>(h, layer, static_cast<const float*>(k), static_cast<const float*>(v), st, pd);
 }
 
 cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, const void* k,
@@ -875,9 +1010,9 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
     s = L.s;
   }
   const bool ok = h->cfg.dtype == CASCADE_BF16
-                      ? launch_maintenance<__nv_bfloat16>(h, g, L, up, static_cast<const __nv_bfloat16*>(k),
+                      ? launch_maintenance<__nv_bfloat16>(h, g, L, up, h->plan, static_cast<const __nv_bfloat16*>(k),
                                                           static_cast<const __nv_bfloat16*>(v), s, false, st)
-                      : launch_maintenance<float>(h, g, L, up, static_cast<const float*>(k),
+                      : launch_maintenance<float>(h, g, L, up, h->plan, static_cast<const float*>(k),
                                                   static_cast<const float*>(v), s, false, st);
   if (!ok || !launches_ok()) return poison(h);
   h->mirrors[layer] = next;
@@ -901,6 +1036,7 @@ cascade_status cascade_last_scores(cascade_handle* h, int32_t layer, float* out,
 cascade_status cascade_reset(cascade_handle* h, int32_t layer, void* stream) {
   if (!h || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
   if (h->poisoned) return CASCADE_ERR_POISONED;
+  if (h->pending[layer].active) return CASCADE_ERR_ORDER;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   if (cudaMemsetAsync(L.mu, 0, h->sz.mu, st) != cudaSuccess ||
@@ -945,9 +1081,50 @@ cascade_status cascade_profile_read(cascade_handle* h, double* ms, int64_t* coun
   return CASCADE_OK;
 }
 
+cascade_status cascade_load_state(cascade_handle* h, int32_t layer, const cascade_state_view* src, void* stream) {
+  if (!h || !src || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (h->poisoned) return CASCADE_ERR_POISONED;
+  if (h->pending[layer].active) return CASCADE_ERR_ORDER;
+  (void)cudaGetLastError();
+  const cascade_config& c = h->cfg;
+  if (src->num_cascades != h->N || src->sub_cache_size != h->c || src->sink_size != h->alpha ||
+      src->slots_total != h->S_tot || src->head_dim != c.head_dim || src->dtype != c.dtype ||
+      src->batch != c.batch || src->num_kv_heads != c.num_kv_heads)
+    return CASCADE_ERR_CONFIG;
+  if (!src->k_raw || !src->v || !src->mu || !src->origin) return CASCADE_ERR_INVALID_ARG;
+  // the mirror must be one Alg. 2 can reach: sinks fill first, a sub-cache that is not
+  // full holds slots [0, count) with xi = count, the counters fit the stream so far
+  const cascade_mirror& mr = src->mirror;
+  int64_t n = mr.sink_count;
+  if (mr.sink_count < 0 || mr.sink_count > h->alpha) return CASCADE_ERR_INVALID_ARG;
+  for (int i = 0; i < CASCADE_MAX_LEVELS; ++i) {
+    const int32_t cnt = mr.counts[i], xi = mr.xi[i];
+    if (i >= h->N) { if (cnt || xi) return CASCADE_ERR_INVALID_ARG; continue; }
+    if (cnt < 0 || cnt > h->c || xi < 0 || xi >= h->c) return CASCADE_ERR_INVALID_ARG;
+    if (cnt < h->c && xi != cnt % h->c) return CASCADE_ERR_INVALID_ARG;
+    if (cnt > 0 && mr.sink_count < h->alpha) return CASCADE_ERR_INVALID_ARG;
+    n += cnt;
+  }
+  if (mr.t < n) return CASCADE_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerBufs& L = h->layers[layer];
+  const size_t rows = (size_t)c.batch * c.num_kv_heads * h->S_tot;
+  const size_t row_bytes = (size_t)c.head_dim * elem_size(c.dtype);
+  if (cudaMemcpyAsync(L.k_raw, src->k_raw, rows * row_bytes, cudaMemcpyDefault, st) != cudaSuccess ||
+      cudaMemcpyAsync(L.v, src->v, rows * row_bytes, cudaMemcpyDefault, st) != cudaSuccess ||
+      cudaMemcpyAsync(L.mu, src->mu, rows * 8, cudaMemcpyDefault, st) != cudaSuccess ||
+      cudaMemcpyAsync(L.origin, src->origin, rows * 8, cudaMemcpyDefault, st) != cudaSuccess ||
+      cudaMemsetAsync(L.s, 0, h->sz.s, st) != cudaSuccess)
+    return poison(h);   // a partial copy leaves the layer neither old nor new
+  h->mirrors[layer] = mr;
+  h->m_last[layer] = 0;
+  return CASCADE_OK;
+}
+
 cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out, void* stream) {
   if (!h || !out || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
   if (h->poisoned) return CASCADE_ERR_POISONED;
+  if (h->pending[layer].active) return CASCADE_ERR_ORDER;
   (void)cudaGetLastError();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];

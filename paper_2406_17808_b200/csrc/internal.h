@@ -165,9 +165,13 @@ struct DecodeParams {
 };
 int decode_gm(int G);
 size_t decode_nsplit(const DecodeParams& p);   // 0: logits of the cache do not fit in TMEM
-cudaError_t launch_decode(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                          int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
-                          cudaStream_t st);
+// the fused cluster kernel (p.update: fold + insertion in-kernel, else s only)
+cudaError_t launch_decode_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
+                                const int32_t* phase_begin_dev, int32_t n_phase, __nv_bfloat16* out,
+                                const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st);
+// fold + selection + moves from s (the commit of a decode attend without inline update)
+cudaError_t launch_decode_commit(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
+                                 const int32_t* phase_begin_dev, int32_t n_phase, cudaStream_t st);
 
 size_t attn_fwd_tc_smem(int d);
 

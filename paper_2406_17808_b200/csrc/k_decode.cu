@@ -671,21 +671,18 @@ cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel
   return cudaLaunchKernelEx(&cfg, kern, tk, tv, p, pl, n_sel, phase_begin_dev, n_phase, out);
 }
 
-cudaError_t launch_decode(const DecodeParams& p_in, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
-                          int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
-                          cudaStream_t st) {
-  DecodeParams p = p_in;
-  p.update = p.homogeneous ? 0 : 1;
+cudaError_t launch_decode_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
+                                const int32_t* phase_begin_dev, int32_t n_phase, __nv_bfloat16* out,
+                                const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
   const int GM = decode_gm(p.G);
-  cudaError_t e;
-  if (GM == 1) e = launch_fused<1>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  else if (GM == 2) e = launch_fused<2>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  else if (GM == 4) e = launch_fused<4>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  else e = launch_fused<8>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  if (e != cudaSuccess || !p.homogeneous) return e;
-  // homogeneous head policy: one reduction per sequence over its kv-heads' s, then the
-  // fold / selections / moves from the reduced s
-  launch_head_homogenize(p.B, p.Hkv, p.S_tot + 1, p.head_reduce, p.s, st);
+  if (GM == 1) return launch_fused<1>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  if (GM == 2) return launch_fused<2>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  if (GM == 4) return launch_fused<4>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  return launch_fused<8>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+}
+
+cudaError_t launch_decode_commit(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
+                                 const int32_t* phase_begin_dev, int32_t n_phase, cudaStream_t st) {
   decode_update_kernel<128><<<p.B * p.Hkv, 256, 0, st>>>(p, pl, n_sel, phase_begin_dev, n_phase);
   return cudaGetLastError();
 }

@@ -44,3 +44,35 @@ def gather_heads(out_shard: torch.Tensor, world: int, buf: torch.Tensor | None =
     if not assemble:
         return buf
     return buf.permute(1, 2, 0, 3, 4).reshape(B, m, world * hq, d)
+
+
+def homogeneous_step(cas, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                     out: torch.Tensor | None = None, group=None, reduce: str = "max", stream=None) -> torch.Tensor:
+    """One Alg. 1 step under the homogeneous head policy with kv-head sharding.
+
+    Homogeneous heads take ONE selection decision per sequence from s reduced over all kv-heads,
+    which now live on different ranks: the library's split step computes the attention and the
+    per-key mass reduced over the LOCAL kv-heads (cascade_attend), the ranks reduce that score
+    buffer in place with an all_reduce (max; mean = sum of the equal-sized local means / world),
+    and cascade_commit folds the global s and inserts the chunk.  m = 1 (q [B, 1, Hq/N, d]) is a
+    decode step."""
+    out = cas.attend(layer, q, k, v, out=out, stream=stream)
+    s = cas.score_buffer(layer)
+    with torch.cuda.stream(stream) if stream is not None else _null():
+        if reduce == "max":
+            dist.all_reduce(s, op=dist.ReduceOp.MAX, group=group)
+        elif reduce == "mean":
+            dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+            s.div_(dist.get_world_size(group))
+        else:
+            raise ValueError(reduce)
+    cas.commit(layer, k, v, stream=stream)
+    return out
+
+
+class _null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False

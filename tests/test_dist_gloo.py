@@ -85,3 +85,50 @@ def test_shard_range_rejects_uneven_split():
     assert shard_range(1, 4, 32, 8) == (slice(8, 16), slice(2, 4))
     with pytest.raises(ValueError):
         shard_range(0, 3, 32, 8)
+
+
+def _homog_worker(rank, world, port, result_q):
+    """Rank r computes its kv-head shard's per-key masses with the oracle (independent policy,
+    max over each GQA group), reduces them over its local kv-heads, then all_reduce(MAX) over the
+    ranks -- the reduction dist.homogeneous_step applies to the library's score buffer."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.model import CascadeOracle, OracleConfig
+    from paper_2406_17808_b200.dist import shard_range
+    from paper_2406_17808_b200.synth import Synth
+    B, Hq, Hkv, d, m = 1, 8, 4, 16, 6
+    syn = Synth(B, Hq, Hkv, d, seed=33, dtype=torch.float32)
+    qs, ks = shard_range(rank, world, Hq, Hkv)
+    orc = CascadeOracle(OracleConfig(1, B, Hq // world, Hkv // world, d, 2, 8, 2, gamma=0.9))
+    q, k, v = syn.chunk(0, m)
+    _, s = orc.prefill_stride(0, q[:, :, qs].double().numpy(), k[:, :, ks].double().numpy(),
+                              v[:, :, ks].double().numpy())
+    local = torch.from_numpy(s.max(axis=1))                 # [B, S_tot + m]: max over local kv-heads
+    dist.all_reduce(local, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        result_q.put(local.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_homogeneous_reduction_across_ranks_is_the_all_heads_max():
+    from oracle.model import CascadeOracle, OracleConfig
+    from paper_2406_17808_b200.synth import Synth
+    world = 2
+    ctx = mp.get_context("spawn")
+    q_ = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_homog_worker, args=(r, world, port, q_)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q_.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    B, Hq, Hkv, d, m = 1, 8, 4, 16, 6
+    syn = Synth(B, Hq, Hkv, d, seed=33, dtype=torch.float32)
+    hom = CascadeOracle(OracleConfig(1, B, Hq, Hkv, d, 2, 8, 2, gamma=0.9, head_policy="homogeneous"))
+    q, k, v = syn.chunk(0, m)
+    _, s = hom.prefill_stride(0, q.double().numpy(), k.double().numpy(), v.double().numpy())
+    np.testing.assert_array_equal(got, s[:, 0])
