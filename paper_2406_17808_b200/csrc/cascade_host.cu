@@ -106,8 +106,8 @@ Sizes compute_sizes(const cascade_config& c) {
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
                 z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
-  z.tab_hi = align_up(((S + M) / 32 + 1) * (d / 2) * sizeof(double2));
-  z.tab_lo = align_up(32 * (d / 2) * sizeof(double2));
+  z.tab_hi = align_up(((S + M) / 32 + 1) * d * sizeof(float2));   // [a][hi parts | lo parts]
+  z.tab_lo = align_up(32 * d * sizeof(float2));
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
@@ -162,8 +162,8 @@ struct cascade_handle {
   std::vector<int32_t> m_last;
   std::vector<Pending> pending;   // per layer: an attend awaiting its commit
   double2* rope_tab;     // [S_tot + max_stride][d/2] (cos, sin)(pos theta_i) in fp64
-  double2* tab_hi;       // [npos/32 + 1][d/2] (cos, sin)(32 a theta_i), fp64 (decode angle addition)
-  double2* tab_lo;       // [32][d/2] (cos, sin)(b theta_i), fp64
+  float2* tab_hi;        // [npos/32 + 1][d] (cos, sin)(32 a theta_i) double-float: [d/2 hi | d/2 lo]
+  float2* tab_lo;        // [32][d] (cos, sin)(b theta_i) double-float: [d/2 hi | d/2 lo]
   void *stage_q, *stage_k, *stage_v, *stage_out;           // set 0 (aliases stage[0])
   struct Stage { void *q, *k, *v, *out; } stage[2];
   // pipelined host path (cascade_prefill_stride_host_async): copy streams and per-set events
@@ -349,8 +349,8 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.maint_barrier = 0;
   }
   h->rope_tab = reinterpret_cast<double2*>(take(sz.rope_tab));
-  h->tab_hi = reinterpret_cast<double2*>(take(sz.tab_hi));
-  h->tab_lo = reinterpret_cast<double2*>(take(sz.tab_lo));
+  h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
+  h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
   for (int i = 0; i < 2; ++i) {
     h->stage[i].q = take(sz.stage_q); h->stage[i].k = take(sz.stage_kv);
     h->stage[i].v = take(sz.stage_kv); h->stage[i].out = take(sz.stage_out);
@@ -416,16 +416,20 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
                           cudaMemcpyHostToDevice) == cudaSuccess;
     // angle-addition factors for decode: pe = 32 a + b, cos/sin(32 a theta_i) and cos/sin(b theta_i)
     const size_t nhi = npos / 32 + 1;
-    std::vector<double2> hi(nhi * half), lo(32 * half);
+    std::vector<float2> hi(nhi * 2 * half), lo(32 * 2 * half);
+    auto split = [&](float2* row, int i, double a) {   // (cos, sin)(a) as fp32 hi + fp32 lo
+      const double c = std::cos(a), s = std::sin(a);
+      const float ch = (float)c, sh = (float)s;
+      row[i] = make_float2(ch, sh);
+      row[half + i] = make_float2((float)(c - (double)ch), (float)(s - (double)sh));
+    };
     for (int i = 0; i < half; ++i) {
       const double f = std::pow(cfg->rope_theta, -(2.0 * i) / cfg->head_dim);
-      for (size_t a = 0; a < nhi; ++a)
-        hi[a * half + i] = make_double2(std::cos((double)(32 * a) * f), std::sin((double)(32 * a) * f));
-      for (int bb = 0; bb < 32; ++bb)
-        lo[bb * half + i] = make_double2(std::cos((double)bb * f), std::sin((double)bb * f));
+      for (size_t a = 0; a < nhi; ++a) split(&hi[a * 2 * half], i, (double)(32 * a) * f);
+      for (int bb = 0; bb < 32; ++bb) split(&lo[bb * 2 * half], i, (double)bb * f);
     }
-    ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(double2), cudaMemcpyHostToDevice) == cudaSuccess;
-    ok = ok && cudaMemcpy(h->tab_lo, lo.data(), lo.size() * sizeof(double2), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->tab_hi, hi.data(), hi.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->tab_lo, lo.data(), lo.size() * sizeof(float2), cudaMemcpyHostToDevice) == cudaSuccess;
   }
   ok = ok && cudaDeviceSynchronize() == cudaSuccess;
   if (!ok) { cascade_destroy(h); return CASCADE_ERR_CUDA; }
@@ -777,7 +781,7 @@ cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat
   dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
   dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
   dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
-  dp.tab = h->rope_tab; dp.tab_hi64 = h->tab_hi; dp.tab_lo64 = h->tab_lo;
+  dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
   dp.n_tiles = up.n_dec_tiles;
   dp.dec_tiles = up.dec_tiles;
   dp.nsplit = (int32_t)decode_nsplit(dp);

@@ -160,8 +160,8 @@ struct DecodeParams {
   int64_t* origin;              // state
   float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
   const double2* tab;           // [npos][D/2] cos/sin(pe theta_i), fp64
-  const double2* tab_hi64;      // [npos/32 + 1][D/2] cos/sin(32 a theta_i), fp64
-  const double2* tab_lo64;      // [32][D/2] cos/sin(b theta_i), fp64
+  const float2* tab_hi;         // [npos/32 + 1][D] cos/sin(32 a theta_i) double-float [D/2 hi | D/2 lo]
+  const float2* tab_lo;         // [32][D] cos/sin(b theta_i) double-float [D/2 hi | D/2 lo]
 };
 int decode_gm(int G);
 size_t decode_nsplit(const DecodeParams& p);   // 0: logits of the cache do not fit in TMEM

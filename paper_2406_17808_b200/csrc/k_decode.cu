@@ -24,11 +24,13 @@
 // across clusters: the fused kernel then only writes s, and decode_update_kernel folds, selects
 // and moves after head_homogenize_kernel.
 //
-// Rotation precision (reading Q17): the key operand is the bf16 rounding of R(pe) k with the
-// rotation in float64 -- cos/sin((32 a + b) theta_i) by angle addition from two float64 tables
-// (a-rows staged per tile, b-rows resident), products and sums in double, rounded double ->
-// float -> bf16 -- so the operand is the oracle's bf16 value (its float64 rotation rounded the
-// same way) up to a ~1e-16 relative difference in cos/sin.
+// Rotation precision (reading Q17): the key operand must be the bf16 rounding of the exact R(pe) k
+// (the oracle's float64 rotation rounded double -> float -> bf16; rope_prep computes exactly that).
+// Per element the kernel rotates in fp32 (angle addition from the fp32 hi parts of double-float
+// tables) and proves from an error bound that the bf16 rounding cannot differ; the rare elements
+// it cannot prove (~1.5e-3 of the pairs) are recomputed in double (cos / sin from hi + lo parts by
+// angle addition, then rope_prep's double products and double -> float rounding).  (Rotating everything in
+// float64 measured 1.21 vs 0.89 ms per configs[3] step: the DMUL / F2F issue of two warpgroups.)
 #include "common.cuh"
 
 #include <cmath>
@@ -39,10 +41,10 @@ namespace cascade {
 namespace {
 constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
 constexpr int kLoRows = 32;                                  // pe = 32 a + b
-constexpr int kRowBytes = 64 * 16;                           // 64 rotate-half pairs x double2
-constexpr int kLoStride = kRowBytes + 16;                    // padded bytes per b-row (bank spread)
+constexpr int kRowBytes = 128 * 8;                           // a-row: 64 float2 (cos, sin) hi parts | 64 lo parts
+constexpr int kLoStride = 64 * 8 + 8;                        // padded bytes per b-row (bank spread)
 constexpr int kKStages = 3, kVStages = 2;
-constexpr int kKStageBytes = 32768 + kHiRows * kRowBytes;    // 37888: K tile + a-rows, 1 KB multiple
+constexpr int kKStageBytes = (32768 + kHiRows * kRowBytes + 1023) / 1024 * 1024;   // K tile + a-rows
 constexpr int kVStageBytes = 32768;
 constexpr uint32_t kColLg = 64;                              // compact logits: GM columns per tile
 constexpr uint32_t kTmemCols = 512;
@@ -50,7 +52,7 @@ constexpr uint32_t kTmemCols = 512;
 
 size_t decode_fused_smem(int GM) {
   return (size_t)kKStages * kKStageBytes + (size_t)kVStages * kVStageBytes + 4096 + 4096 +
-         (size_t)kLoRows * kLoStride + (size_t)GM * 128 * 4 + 4 * 8 * 4 + 40 * 4 + 64 + 24 * 8 + 1024;
+         2 * (size_t)kLoRows * kLoStride + (size_t)GM * 128 * 4 + 4 * 8 * 4 + 40 * 4 + 64 + 24 * 8 + 1024;
 }
 int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 
@@ -81,8 +83,9 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   uint8_t* sV = sK + kKStages * kKStageBytes;               // kVStages x V
   uint8_t* sQ = sV + kVStages * kVStageBytes;               // [16 rows x 128 d] SW128 (2 x 2 KB)
   uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
-  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i), fp64
-  float* sO = reinterpret_cast<float*>(sLo + kLoRows * kLoStride);   // [GM][128] scaled partial O
+  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i), fp32 hi parts
+  uint8_t* sLoL = sLo + kLoRows * kLoStride;                // 32 x kLoStride: their fp32 lo parts
+  float* sO = reinterpret_cast<float*>(sLoL + kLoRows * kLoStride);  // [GM][128] scaled partial O
   float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sO + GM * 128);  // [4][8]
   float* sML = reinterpret_cast<float*>(sRed + 4);          // [0, 8) max, [8, 16) sum, [16, 24) lse2
   float* sCorr = sML + 24;                                  // [8]
@@ -135,8 +138,11 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
     *reinterpret_cast<__nv_bfloat16*>(sQ + off) = __float2bfloat16_rn(r1);
     *reinterpret_cast<__nv_bfloat16*>(sQ + 2048 + off) = __float2bfloat16_rn(r2);
   }
-  for (int o = tid; o < kLoRows * HALF; o += blockDim.x)
-    *reinterpret_cast<double2*>(sLo + (o / HALF) * kLoStride + (o % HALF) * 16) = p.tab_lo64[o];
+  for (int o = tid; o < kLoRows * HALF; o += blockDim.x) {     // tab_lo rows: [64 hi | 64 lo]
+    const int rr = o / HALF, ii = o % HALF;
+    *reinterpret_cast<float2*>(sLo + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + ii];
+    *reinterpret_cast<float2*>(sLoL + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + HALF + ii];
+  }
   for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
           for (int kb = 0; kb < 2; ++kb) tc::tma_load_2d(st + kb * 16384, &tm_k, kfull + s, kb * 64, row);
         }
         for (int r = 0; r < nA; ++r)
-          tc::bulk_load(st + 32768 + r * kRowBytes, p.tab_hi64 + (long long)(a0 + r) * HALF, kRowBytes, kfull + s);
+          tc::bulk_load(st + 32768 + r * kRowBytes, p.tab_hi + (long long)(a0 + r) * 2 * HALF, kRowBytes, kfull + s);
       }
     }
   } else if (warp == 3) {
@@ -242,11 +248,18 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       tc::mbar_wait(kfull + s, (j / kKStages) & 1);
       if (start < p.S_tot) {
         // ---- rotate row t in place: pairs (i, i + 64) live at the same swizzled offset of the
-        //      two 64-column blocks; cos/sin((32a + b) theta_i) by angle addition in double ----
+        //      two 64-column blocks.  Fast path in fp32: cos/sin((32a + b) theta_i) by angle
+        //      addition from fp32 tables (a-rows staged per tile, b-rows resident); its error is
+        //      below 16 * 2^-24 * (|x1| + |x2|) (table rounding, two products, two roundings), so
+        //      its bf16 rounding equals that of the exact rotation unless the fp32 value lies that
+        //      close to a bf16 rounding midpoint -- then (~2e-4 of the elements) the pair is
+        //      recomputed exactly as rope_prep does it: fp64 table, double products, double ->
+        //      float -> bf16 (reading Q17).
         const int hr = (pe >> 5) - (pe0 >> 5);
-        const double2* hi = reinterpret_cast<const double2*>(st + 32768 + (valid ? hr : 0) * kRowBytes);
-        const double2* lo = reinterpret_cast<const double2*>(sLo + (pe & 31) * kLoStride);
-#pragma unroll 1
+        const float2* hi = reinterpret_cast<const float2*>(st + 32768 + (valid ? hr : 0) * kRowBytes);
+        const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
+        const float2* lo_l = reinterpret_cast<const float2*>(sLoL + (pe & 31) * kLoStride);
+#pragma unroll 2
         for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = t * 128 + ((c ^ (t & 7)) << 4);
           uint4* pa = reinterpret_cast<uint4*>(st + off);
@@ -260,13 +273,37 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int i = c * 8 + 2 * e2 + u;
-              const double2 h2 = hi[i], l2 = lo[i];
-              const double cs = fma(h2.x, l2.x, -(h2.y * l2.y));    // cos((32a + b) theta_i)
-              const double sn = fma(h2.y, l2.x, h2.x * l2.y);       // sin((32a + b) theta_i)
-              const double x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
-              const double x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
-              r[u] = __double2float_rn(fma(x1, cs, -(x2 * sn)));
-              r[2 + u] = __double2float_rn(fma(x2, cs, x1 * sn));
+              const float2 h2 = hi[i], l2 = lo[i];
+              const float cs = fmaf(h2.x, l2.x, -(h2.y * l2.y));    // cos((32a + b) theta_i)
+              const float sn = fmaf(h2.y, l2.x, h2.x * l2.y);       // sin((32a + b) theta_i)
+              const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
+              const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
+              float y1 = fmaf(x1, cs, -(x2 * sn));
+              float y2 = fmaf(x2, cs, x1 * sn);
+              // |error| <= 3 * 2^-24 * (|x1| + |x2|): the four table entries (half an ulp each,
+              // |cos|, |sin| <= 1), the product and the fma roundings; bound taken as 4x.  Risky
+              // iff the distance of y to the bf16 rounding midpoint, in fp32 ulps of y
+              // (2^(e - 150)), is within error / ulp = 4 (|x1| + |x2|) 2^(126 - e).
+              const float bound = 4.f * (fabsf(x1) + fabsf(x2));
+              auto risky = [&](float y) {
+                const uint32_t b = __float_as_uint(y);
+                const int e = (int)((b >> 23) & 0xffu);
+                const float mid = fabsf((float)((int)(b & 0xffffu) - 0x8000));
+                return e < 2 || e > 250 || mid <= bound * __uint_as_float((uint32_t)(253 - e) << 23);
+              };
+              if (valid && (risky(y1) || risky(y2))) {
+                // exact: cos / sin from the double-float tables (hi + lo) by angle addition in
+                // double, then rope_prep's arithmetic (double products, double -> float)
+                const float2 h2l = hi[HALF + i], l2l = lo_l[i];
+                const double cA = (double)h2.x + (double)h2l.x, sA = (double)h2.y + (double)h2l.y;
+                const double cB = (double)l2.x + (double)l2l.x, sB = (double)l2.y + (double)l2l.y;
+                const double c64 = cA * cB - sA * sB, s64 = sA * cB + cA * sB;
+                const double d1 = x1, d2 = x2;
+                y1 = __double2float_rn(__dsub_rn(__dmul_rn(d1, c64), __dmul_rn(d2, s64)));
+                y2 = __double2float_rn(__dadd_rn(__dmul_rn(d2, c64), __dmul_rn(d1, s64)));
+              }
+              r[u] = y1;
+              r[2 + u] = y2;
             }
             oa[e2] = tc::pack_bf16(r[0], r[1]);
             ob[e2] = tc::pack_bf16(r[2], r[3]);
