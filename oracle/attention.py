@@ -13,6 +13,10 @@
   coefficient C_EMA = (1 - gamma) * gamma**k, k = m - (r + 1), and the
   column sum over rows of P weighted by C_EMA is the key's mass s.
   Heads are independent per KV group and reduced with max (Q7).
+* ``key_mass_onepass``  Alg. 3 as the paper writes it, in its tile
+  order: the normaliser of the column sum at inner step j is the running row sum
+  extrapolated over the remaining steps, l_i + l_i * rho / gamma (reading
+  Q6b: gamma = inner steps completed including step j, rho = steps remaining).
 """
 
 from __future__ import annotations
@@ -136,3 +140,42 @@ def gamma_pow(gamma: float, m: int) -> float:
         base = base * base
         e >>= 1
     return result
+
+
+def key_mass_onepass(q_rot: np.ndarray, k_rot: np.ndarray, n_cached: int, scale: float, gamma: float,
+                     key_tiles, q_tile: int = 128):
+    """Alg. 3 step by step, in the order of its two loops.
+
+    q_rot [m, d]; k_rot [n_cached + m, d] (rows [0, n_cached) the cache, n_cached + r the
+    chunk's keys).  key_tiles: the cache's key tiles in loop order, each a list of row indices
+    into k_rot; the chunk's own keys follow as tiles of q_tile keys (a query block sees the chunk
+    tiles up to its own, causally masked inside the diagonal one).  For query block i and inner
+    step j over its n_i visible key tiles:
+        S_ij = Q_i K_j^T * scale                                  (masked entries -inf)
+        m_i  = max(m_i, rowmax S_ij);  l_i = l_i exp(m_old - m_i) + rowsum exp(S_ij - m_i)
+        S^_ij = exp(S_ij - m_i)                                   (max-adjusted, unnormalised)
+        C_EMA = (1 - gamma) gamma^(m - (r + 1)) per query row r
+        score[K_j] += col_sum( S^_ij / (l_i + l_i rho / gamma_) * C_EMA ),
+            gamma_ = j + 1 (steps completed), rho = n_i - (j + 1) (steps remaining)
+    Returns s [n_cached + m]."""
+    m = q_rot.shape[0]
+    s = np.zeros(k_rot.shape[0])
+    c_ema = ema_weights(m, gamma)
+    chunk_tiles = [list(range(n_cached + t0, n_cached + min(m, t0 + q_tile))) for t0 in range(0, m, q_tile)]
+    for i0 in range(0, m, q_tile):
+        rows = np.arange(i0, min(m, i0 + q_tile))
+        tiles = list(key_tiles) + chunk_tiles[: i0 // q_tile + 1]
+        n_i = len(tiles)
+        m_i = np.full(len(rows), -np.inf)
+        l_i = np.zeros(len(rows))
+        for j, cols in enumerate(tiles):
+            cols = np.asarray(cols)
+            S = (q_rot[rows] @ k_rot[cols].T) * scale
+            S = np.where(cols[None, :] <= n_cached + rows[:, None], S, -np.inf)   # causal in the chunk
+            m_new = np.maximum(m_i, S.max(axis=1))
+            l_i = l_i * np.exp(m_i - m_new) + np.exp(S - m_new[:, None]).sum(axis=1)
+            m_i = m_new
+            S_hat = np.exp(S - m_i[:, None])
+            gamma_, rho = j + 1, n_i - (j + 1)
+            s[cols] += ((S_hat / (l_i + l_i * rho / gamma_)[:, None]) * c_ema[rows][:, None]).sum(axis=0)
+    return s

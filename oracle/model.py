@@ -28,7 +28,7 @@ from typing import Dict, List
 
 import numpy as np
 
-from .attention import chunk_attention, gamma_pow, key_mass, reduce_heads, rope, round_bf16
+from .attention import chunk_attention, gamma_pow, key_mass, key_mass_onepass, reduce_heads, rope, round_bf16
 from .cascade import CascadeHead, Token
 
 
@@ -55,6 +55,13 @@ class OracleConfig:
     # products consume, held in bf16 (the model dtype the paper's kernel runs in); the
     # oracle rounds them to bf16 (round-to-nearest-even) before its float64 dot products.
     round_operands: str = ""          # "" or "bf16"
+    # per-key mass (Alg. 3): "exact" (reading Q6: the final LSE, two passes) or "onepass" (the
+    # paper's own estimator, in the tile order of ``key_mass_onepass``: the cache's
+    # occupied runs in flat-slot order -- sinks, then sub-caches 1..N -- cut into `tile`-slot
+    # tiles, then the chunk's keys in tiles of `tile`).  Decode steps (``decode``) keep the exact
+    # mass in both modes (the single-token kernel knows the final LSE before it writes a mass).
+    score_mode: str = "exact"
+    tile: int = 128
 
     @property
     def c(self) -> int:
@@ -109,8 +116,22 @@ class CascadeOracle:
                                  v=np.array(v_rows[r], dtype=np.float64), mu=mu_new))
 
     # ------------------------------------------------------------------ API
+    def _key_tiles(self, head: CascadeHead, key_slot) -> list:
+        """The cache's key tiles for the one-pass estimator, as row indices of the logical-order
+        key array: each occupied run of flat slots (sinks, sub-cache 1, ..., sub-cache N) cut
+        into tiles of cfg.tile consecutive slots from the run's start."""
+        cfg = self.cfg
+        row_of = {x: r for r, x in enumerate(key_slot) if x < cfg.s_tot}
+        runs = [(0, len(head.sink))] + [(cfg.sink_size + i * cfg.c, ring.count)
+                                        for i, ring in enumerate(head.rings)]
+        tiles = []
+        for start, n in runs:
+            for o in range(0, n, cfg.tile):
+                tiles.append([row_of[start + x] for x in range(o, min(n, o + cfg.tile))])
+        return tiles
+
     def prefill_stride(self, layer: int, q: np.ndarray, k: np.ndarray, v: np.ndarray,
-                       return_heads: bool = False):
+                       return_heads: bool = False, exact_mass: bool = False):
         """One Alg. 1 step. q [B,m,Hq,d], k/v [B,m,Hkv,d] (pre-RoPE). Returns (O [B,m,Hq,d], s [B,Hkv,S_tot+m])."""
         cfg = self.cfg
         B, m, Hq, d = q.shape
@@ -142,7 +163,13 @@ class CascadeOracle:
                         q_rot = round_bf16(q_rot)
                     o_h, P = chunk_attention(q_rot, k_rot, v_all, n_c, cfg.scale)
                     O[b, :, h] = o_h
-                    s_h[j] = key_mass(P, cfg.gamma)
+                    if cfg.score_mode == "exact" or exact_mass:
+                        s_h[j] = key_mass(P, cfg.gamma)
+                    elif cfg.score_mode == "onepass":
+                        s_h[j] = key_mass_onepass(q_rot, k_rot, n_c, cfg.scale, cfg.gamma,
+                                                  self._key_tiles(head, key_slot), cfg.tile)
+                    else:
+                        raise ValueError(cfg.score_mode)
                     s_heads_out[b, h, key_slot] = s_h[j]
                 s_g = reduce_heads(s_h, G, cfg.head_reduce)[0]
                 s_out[b, g, key_slot] = s_g
@@ -158,7 +185,7 @@ class CascadeOracle:
 
     def decode(self, layer: int, q: np.ndarray, k: np.ndarray, v: np.ndarray):
         """Eq. 2 + update: the m = 1 case. q [B,Hq,d], k/v [B,Hkv,d]."""
-        O, s = self.prefill_stride(layer, q[:, None], k[:, None], v[:, None])
+        O, s = self.prefill_stride(layer, q[:, None], k[:, None], v[:, None], exact_mass=True)
         return O[:, 0], s
 
     def update_with_scores(self, layer: int, k: np.ndarray, v: np.ndarray, s_flat: np.ndarray) -> None:

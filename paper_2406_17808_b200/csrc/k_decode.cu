@@ -42,7 +42,7 @@ namespace {
 constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
 constexpr int kLoRows = 32;                                  // pe = 32 a + b
 constexpr int kRowBytes = 128 * 8;                           // a-row: 64 float2 (cos, sin) hi parts | 64 lo parts
-constexpr int kLoStride = 64 * 8 + 8;                        // padded bytes per b-row (bank spread)
+constexpr int kLoStride = 64 * 8 + 16;                       // padded bytes per b-row (16-B aligned, bank spread)
 constexpr int kKStages = 3, kVStages = 2;
 constexpr int kKStageBytes = (32768 + kHiRows * kRowBytes + 1023) / 1024 * 1024;   // K tile + a-rows
 constexpr int kVStageBytes = 32768;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         const float2* hi = reinterpret_cast<const float2*>(st + 32768 + (valid ? hr : 0) * kRowBytes);
         const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
         const float2* lo_l = reinterpret_cast<const float2*>(sLoL + (pe & 31) * kLoStride);
-#pragma unroll 2
+#pragma unroll 1
         for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = t * 128 + ((c ^ (t & 7)) << 4);
           uint4* pa = reinterpret_cast<uint4*>(st + off);
@@ -268,45 +268,50 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
           const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w}, wb[4] = {ub.x, ub.y, ub.z, ub.w};
           uint32_t oa[4], ob[4];
 #pragma unroll
-          for (int e2 = 0; e2 < 4; ++e2) {
-            float r[4];
+          for (int e2 = 0; e2 < 4; ++e2) {          // pairs i0, i0 + 1 as packed fp32x2 lanes
+            const int i0 = c * 8 + 2 * e2;
+            const float4 hh = *reinterpret_cast<const float4*>(hi + i0);   // c_i, s_i, c_i+1, s_i+1
+            const float4 ll = *reinterpret_cast<const float4*>(lo + i0);
+            const float2 cA = make_float2(hh.x, hh.z), sA = make_float2(hh.y, hh.w);
+            const float2 cB = make_float2(ll.x, ll.z), sB = make_float2(ll.y, ll.w);
+            const float2 cs = __ffma2_rn(cA, cB, __fmul2_rn(sA, make_float2(-sB.x, -sB.y)));   // cos(A + B)
+            const float2 sn = __ffma2_rn(sA, cB, __fmul2_rn(cA, sB));                         // sin(A + B)
+            const float2 x1 = make_float2(__uint_as_float(wa[e2] << 16), __uint_as_float(wa[e2] & 0xffff0000u));
+            const float2 x2 = make_float2(__uint_as_float(wb[e2] << 16), __uint_as_float(wb[e2] & 0xffff0000u));
+            const float2 y1 = __ffma2_rn(x1, cs, __fmul2_rn(make_float2(-x2.x, -x2.y), sn));  // x1 c - x2 s
+            const float2 y2 = __ffma2_rn(x2, cs, __fmul2_rn(x1, sn));                         // x2 c + x1 s
+            // |y - exact| <= 3 * 2^-24 (|x1| + |x2|) (four table entries at half an ulp, |cos|,
+            // |sin| <= 1, one product and one fma rounding).  With delta = 4e-7 (|x1| + |x2|)
+            // (> that bound + half an ulp of y), [y - delta, y + delta] holds the exact value, so
+            // when both ends round to the same bf16 so does the exact rotation (rounding is
+            // monotonic) and that bf16 is the result; otherwise the pair is recomputed exactly.
+            const float2 dl = __fmul2_rn(__fadd2_rn(make_float2(fabsf(x1.x), fabsf(x1.y)),
+                                                    make_float2(fabsf(x2.x), fabsf(x2.y))),
+                                         make_float2(4e-7f, 4e-7f));
+            const float2 nd = make_float2(-dl.x, -dl.y);
+            const float2 y1l = __fadd2_rn(y1, nd), y1h = __fadd2_rn(y1, dl);
+            const float2 y2l = __fadd2_rn(y2, nd), y2h = __fadd2_rn(y2, dl);
+            uint32_t r1 = tc::pack_bf16(y1l.x, y1l.y), r2 = tc::pack_bf16(y2l.x, y2l.y);
+            if (valid && (r1 != tc::pack_bf16(y1h.x, y1h.y) || r2 != tc::pack_bf16(y2h.x, y2h.y))) {
+              // exact: cos / sin from the double-float tables (hi + lo) by angle addition in
+              // double, then rope_prep's arithmetic (double products, double -> float -> bf16)
+              float o1[2], o2[2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int i = c * 8 + 2 * e2 + u;
-              const float2 h2 = hi[i], l2 = lo[i];
-              const float cs = fmaf(h2.x, l2.x, -(h2.y * l2.y));    // cos((32a + b) theta_i)
-              const float sn = fmaf(h2.y, l2.x, h2.x * l2.y);       // sin((32a + b) theta_i)
-              const float x1 = __uint_as_float(u ? (wa[e2] & 0xffff0000u) : (wa[e2] << 16));
-              const float x2 = __uint_as_float(u ? (wb[e2] & 0xffff0000u) : (wb[e2] << 16));
-              float y1 = fmaf(x1, cs, -(x2 * sn));
-              float y2 = fmaf(x2, cs, x1 * sn);
-              // |error| <= 3 * 2^-24 * (|x1| + |x2|): the four table entries (half an ulp each,
-              // |cos|, |sin| <= 1), the product and the fma roundings; bound taken as 4x.  Risky
-              // iff the distance of y to the bf16 rounding midpoint, in fp32 ulps of y
-              // (2^(e - 150)), is within error / ulp = 4 (|x1| + |x2|) 2^(126 - e).
-              const float bound = 4.f * (fabsf(x1) + fabsf(x2));
-              auto risky = [&](float y) {
-                const uint32_t b = __float_as_uint(y);
-                const int e = (int)((b >> 23) & 0xffu);
-                const float mid = fabsf((float)((int)(b & 0xffffu) - 0x8000));
-                return e < 2 || e > 250 || mid <= bound * __uint_as_float((uint32_t)(253 - e) << 23);
-              };
-              if (valid && (risky(y1) || risky(y2))) {
-                // exact: cos / sin from the double-float tables (hi + lo) by angle addition in
-                // double, then rope_prep's arithmetic (double products, double -> float)
-                const float2 h2l = hi[HALF + i], l2l = lo_l[i];
-                const double cA = (double)h2.x + (double)h2l.x, sA = (double)h2.y + (double)h2l.y;
-                const double cB = (double)l2.x + (double)l2l.x, sB = (double)l2.y + (double)l2l.y;
-                const double c64 = cA * cB - sA * sB, s64 = sA * cB + cA * sB;
-                const double d1 = x1, d2 = x2;
-                y1 = __double2float_rn(__dsub_rn(__dmul_rn(d1, c64), __dmul_rn(d2, s64)));
-                y2 = __double2float_rn(__dadd_rn(__dmul_rn(d2, c64), __dmul_rn(d1, s64)));
+              for (int u = 0; u < 2; ++u) {
+                const int i = i0 + u;
+                const float2 h2 = hi[i], h2l = hi[HALF + i], l2 = lo[i], l2l = lo_l[i];
+                const double ca = (double)h2.x + (double)h2l.x, sa = (double)h2.y + (double)h2l.y;
+                const double cb = (double)l2.x + (double)l2l.x, sb = (double)l2.y + (double)l2l.y;
+                const double c64 = ca * cb - sa * sb, s64 = sa * cb + ca * sb;
+                const double d1 = u ? x1.y : x1.x, d2 = u ? x2.y : x2.x;
+                o1[u] = __double2float_rn(__dsub_rn(__dmul_rn(d1, c64), __dmul_rn(d2, s64)));
+                o2[u] = __double2float_rn(__dadd_rn(__dmul_rn(d2, c64), __dmul_rn(d1, s64)));
               }
-              r[u] = y1;
-              r[2 + u] = y2;
+              r1 = tc::pack_bf16(o1[0], o1[1]);
+              r2 = tc::pack_bf16(o2[0], o2[1]);
             }
-            oa[e2] = tc::pack_bf16(r[0], r[1]);
-            ob[e2] = tc::pack_bf16(r[2], r[3]);
+            oa[e2] = r1;
+            ob[e2] = r2;
           }
           *pa = make_uint4(oa[0], oa[1], oa[2], oa[3]);
           *pb = make_uint4(ob[0], ob[1], ob[2], ob[3]);
