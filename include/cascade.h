@@ -115,8 +115,20 @@ typedef struct {
   int32_t selection;     /* 1 = EMA token selection; 0 = the ablation   */
                          /* without it (reading Q3: the resident stays and the */
                          /* carried token is dropped); else CONFIG      */
-  int32_t reserved;
+  int32_t options;       /* bitmask of CASCADE_OPT_* (0: the defaults); unknown    */
+                         /* bits CONFIG                                         */
 } cascade_config;
+
+/* cascade_config.options */
+#define CASCADE_OPT_ONEPASS_SCORES 1     /* per-key mass by the paper's one-pass estimator  */
+                                         /* (Alg. 3 normaliser l + l rho/gamma) in */
+                                         /* prefill instead of the exact two-pass mass;    */
+                                         /* decode stays exact.  bf16 only (else           */
+                                         /* UNSUPPORTED).                                  */
+#define CASCADE_OPT_EXACT_DECODE_ROPE 2  /* decode rotates cached keys with proven-exact   */
+                                         /* bf16 rounding (reading Q17) at ~+45 % decode   */
+                                         /* time; default: fp32 rotation, one bf16 ulp off */
+                                         /* on ~2e-5 of the key elements.                  */
 
 /* Host mirror of one layer's cascade counters (identical for all b, g). */
 typedef struct {

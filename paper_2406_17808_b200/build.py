@@ -17,8 +17,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libcascade.so")
+OBJ = os.environ.get("CASCADE_OBJ_DIR", os.path.join(ROOT, "build", "obj"))
+# CASCADE_LIB (with CASCADE_OBJ_DIR and CASCADE_NVCC_EXTRA) builds an experiment variant elsewhere
+LIB = os.environ.get("CASCADE_LIB", os.path.join(HERE, "libcascade.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

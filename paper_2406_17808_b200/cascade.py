@@ -15,10 +15,12 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcascade.so")
+# CASCADE_LIB selects an experiment build of the same sources (scripts/ A/B runs); default in-tree
+LIB_PATH = os.environ.get("CASCADE_LIB", os.path.join(HERE, "libcascade.so"))
 
 MAX_LEVELS = 16
 F32, BF16 = 0, 1
+OPT_ONEPASS_SCORES, OPT_EXACT_DECODE_ROPE = 1, 2
 _STATUS = {0: "ok", -1: "invalid argument", -2: "invalid config", -3: "bad shape",
            -4: "call out of order", -5: "workspace", -6: "CUDA error", -7: "unsupported",
            -8: "handle poisoned by an earlier CUDA error"}
@@ -39,7 +41,7 @@ class _Config(ctypes.Structure):
                 ("ema_gamma", ctypes.c_double), ("rope_theta", ctypes.c_double),
                 ("softmax_scale", ctypes.c_double), ("head_policy", ctypes.c_int32),
                 ("head_reduce", ctypes.c_int32), ("selection", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("options", ctypes.c_int32)]
 
 
 class Mirror(ctypes.Structure):
@@ -128,6 +130,8 @@ class CascadeConfig:
     head_reduce: str = "max"      # "max"; ablations "mean", "median"
     selection: bool = True        # False: the ablation without token selection (Q3)
     head_policy: str = "independent"   # or "homogeneous": one decision per sequence
+    score_mode: str = "exact"     # or "onepass": the paper's one-pass estimator (Alg. 3)
+    exact_decode_rope: bool = False   # decode key rotation with proven-exact bf16 rounding (Q17)
 
     def c_struct(self) -> _Config:
         return _Config(self.num_layers, self.batch, self.num_q_heads, self.num_kv_heads,
@@ -135,7 +139,9 @@ class CascadeConfig:
                        self.max_stride, BF16 if self.dtype == "bf16" else F32,
                        self.ema_gamma, self.rope_theta, self.softmax_scale,
                        {"independent": 0, "homogeneous": 1}[self.head_policy],
-                       {"max": 0, "mean": 1, "median": 2}[self.head_reduce], int(self.selection), 0)
+                       {"max": 0, "mean": 1, "median": 2}[self.head_reduce], int(self.selection),
+                       {"exact": 0, "onepass": OPT_ONEPASS_SCORES}[self.score_mode] |
+                       (OPT_EXACT_DECODE_ROPE if self.exact_decode_rope else 0))
 
     @property
     def torch_dtype(self):

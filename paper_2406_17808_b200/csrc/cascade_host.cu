@@ -254,6 +254,8 @@ cascade_status cascade_validate_config(const cascade_config* c) {
   if (c->dtype == CASCADE_BF16 && c->num_q_heads / c->num_kv_heads > 8) return CASCADE_ERR_UNSUPPORTED;
   if (c->head_policy < 0 || c->head_policy > 1) return CASCADE_ERR_CONFIG;
   if (c->head_policy == 1 && c->head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;  // median of all heads
+  if (c->options & ~(CASCADE_OPT_ONEPASS_SCORES | CASCADE_OPT_EXACT_DECODE_ROPE)) return CASCADE_ERR_CONFIG;
+  if ((c->options & CASCADE_OPT_ONEPASS_SCORES) && c->dtype != CASCADE_BF16) return CASCADE_ERR_UNSUPPORTED;
   const long long S = (long long)c->sink_size + c->cache_size;
   if (S + c->max_stride > (1LL << 30)) return CASCADE_ERR_CONFIG;
   return CASCADE_OK;
@@ -777,6 +779,7 @@ cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat
   dp.head_reduce = g.head_reduce;
   dp.homogeneous = g.homogeneous;
   dp.update = commit_inline && !g.homogeneous ? 1 : 0;
+  dp.exact_rope = (h->cfg.options & CASCADE_OPT_EXACT_DECODE_ROPE) ? 1 : 0;
   dp.q = q; dp.k_new = k; dp.v_new = v;
   dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
   dp.v_mut = static_cast<__nv_bfloat16*>(L.v);

@@ -151,6 +151,7 @@ struct DecodeParams {
   int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
   int32_t homogeneous;          // head policy: 0 independent, 1 homogeneous
   int32_t update;               // fused kernel: 1 fold + insertion in-kernel; 0 s only (homogeneous)
+  int32_t exact_rope;           // 1: proven-exact bf16 rounding of the rotated keys (Q17)
   const __nv_bfloat16* q;       // [B][Hq][D]   pre-RoPE
   const __nv_bfloat16* k_new;   // [B][Hkv][D]
   const __nv_bfloat16* v_new;   // [B][Hkv][D]

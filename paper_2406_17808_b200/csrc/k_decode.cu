@@ -24,16 +24,19 @@
 // across clusters: the fused kernel then only writes s, and decode_update_kernel folds, selects
 // and moves after head_homogenize_kernel.
 //
-// Rotation precision (reading Q17): the key operand must be the bf16 rounding of the exact R(pe) k
-// (the oracle's float64 rotation rounded double -> float -> bf16; rope_prep computes exactly that).
-// Per element the kernel rotates in fp32 (angle addition from the fp32 hi parts of double-float
-// tables) and proves from an error bound that the bf16 rounding cannot differ; the rare elements
-// it cannot prove (~1.5e-3 of the pairs) are recomputed in double (cos / sin from hi + lo parts by
-// angle addition, then rope_prep's double products and double -> float rounding).  (Rotating everything in
+// Rotation precision (reading Q17): the oracle's key operand is the bf16 rounding of the exact R(pe) k
+// (its float64 rotation rounded double -> float -> bf16; rope_prep computes exactly that).  The
+// decode kernel rotates in fp32 on packed fp32x2 lanes (angle addition from the fp32 hi parts of
+// double-float tables): error <= 3 * 2^-24 (|x1| + |x2|), so its bf16 rounding differs from the
+// exact one for ~2e-5 of the elements (by one bf16 ulp of one coordinate).  With
+// CASCADE_OPT_EXACT_DECODE_ROPE the kernel proves each rounding with an interval check and
+// recomputes the unprovable pairs (~2e-3 of them) in double from the double-float tables -- exact
+// operands, at ~+45 % decode time (the divergent fixups), so it is the parity mode, not the default.  (Rotating everything in
 // float64 measured 1.21 vs 0.89 ms per configs[3] step: the DMUL / F2F issue of two warpgroups.)
 #include "common.cuh"
 
 #include <cmath>
+#include <type_traits>
 #include "tc_util.cuh"
 
 namespace cascade {
@@ -41,19 +44,29 @@ namespace cascade {
 namespace {
 constexpr int kHiRows = 5;                                   // a-rows per tile: 128 consecutive pe span <= 5
 constexpr int kLoRows = 32;                                  // pe = 32 a + b
-constexpr int kRowBytes = 128 * 8;                           // a-row: 64 float2 (cos, sin) hi parts | 64 lo parts
 constexpr int kLoStride = 64 * 8 + 16;                       // padded bytes per b-row (16-B aligned, bank spread)
-constexpr int kKStages = 3, kVStages = 2;
-constexpr int kKStageBytes = (32768 + kHiRows * kRowBytes + 1023) / 1024 * 1024;   // K tile + a-rows
-constexpr int kVStageBytes = 32768;
+constexpr int kKStages = 3;
+constexpr int kTileBytes32K = 32768;                         // one 128 x 128 bf16 K or V tile
 constexpr uint32_t kColLg = 64;                              // compact logits: GM columns per tile
 constexpr uint32_t kTmemCols = 512;
+// EXACT: the rotation proves every bf16 rounding and recomputes the unprovable pairs from the
+// double-float tables, which needs the tables' lo parts in shared memory (a-rows of 1 KB, a second
+// b-row table) and leaves room for two V stages; the fast variant stages hi parts only, three V stages.
+template <bool EXACT> struct DecLayout {
+  static constexpr int kVStages = EXACT ? 2 : 3;
+  static constexpr int kRowBytes = EXACT ? 1024 : 512;      // a-row: [64 float2 hi | 64 float2 lo] or hi only
+  static constexpr int kARows = kHiRows * kRowBytes;        // a-rows per K stage
+  static constexpr int kLoTables = EXACT ? 2 : 1;
+  // sK | sV | sQ | sP | sA | sLo (| sLoL) | scalars + barriers; sO aliases sQ / sP after the tiles
+  static constexpr size_t smem(int GM) {
+    return (size_t)kKStages * kTileBytes32K + (size_t)kVStages * kTileBytes32K + 4096 + 4096 +
+           (size_t)kKStages * kARows + (size_t)kLoTables * kLoRows * kLoStride + 4 * 8 * 4 + 40 * 4 + 64 +
+           24 * 8 + 1024;
+  }
+};
 }  // namespace
 
-size_t decode_fused_smem(int GM) {
-  return (size_t)kKStages * kKStageBytes + (size_t)kVStages * kVStageBytes + 4096 + 4096 +
-         2 * (size_t)kLoRows * kLoStride + (size_t)GM * 128 * 4 + 4 * 8 * 4 + 40 * 4 + 64 + 24 * 8 + 1024;
-}
+size_t decode_fused_smem(int GM, bool exact) { return exact ? DecLayout<true>::smem(GM) : DecLayout<false>::smem(GM); }
 int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 
 // Tensor-core decode, warp roles (512 threads):
@@ -70,23 +83,26 @@ int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 // and its warp 0 applies the insertion.
 // Tile descriptor (int4, host): start slot, length, pe of key 0 (pe of key j = pe0 + j: the host
 // splits a tile where a full ring wraps past its oldest slot).
-template <int GM>
+template <int GM, bool EXACT>
 __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                               const __grid_constant__ CUtensorMap tm_v,
                                                               DecodeParams p, PlanDev pl, int32_t n_sel,
                                                               const int32_t* __restrict__ phase_begin,
                                                               int32_t n_phase, __nv_bfloat16* __restrict__ out) {
   constexpr int D = 128, HALF = 64;
+  using Lay = DecLayout<EXACT>;
+  constexpr int kVStages = Lay::kVStages, kRowBytes = Lay::kRowBytes;
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
-  uint8_t* sK = dsm;                                        // kKStages x [K | a-rows]
-  uint8_t* sV = sK + kKStages * kKStageBytes;               // kVStages x V
-  uint8_t* sQ = sV + kVStages * kVStageBytes;               // [16 rows x 128 d] SW128 (2 x 2 KB)
+  uint8_t* sK = dsm;                                        // kKStages x K tile (1 KB aligned for TMA)
+  uint8_t* sV = sK + kKStages * kTileBytes32K;              // kVStages x V tile
+  uint8_t* sQ = sV + kVStages * kTileBytes32K;              // [16 rows x 128 d] SW128 (2 x 2 KB)
   uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
-  uint8_t* sLo = sP + 4096;                                 // 32 x kLoStride: cos/sin(b theta_i), fp32 hi parts
-  uint8_t* sLoL = sLo + kLoRows * kLoStride;                // 32 x kLoStride: their fp32 lo parts
-  float* sO = reinterpret_cast<float*>(sLoL + kLoRows * kLoStride);  // [GM][128] scaled partial O
-  float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sO + GM * 128);  // [4][8]
+  uint8_t* sA = sP + 4096;                                  // kKStages x the tile's a-rows (cos/sin(32a theta))
+  uint8_t* sLo = sA + kKStages * Lay::kARows;               // 32 x kLoStride: cos/sin(b theta_i), fp32 hi parts
+  uint8_t* sLoL = sLo + (EXACT ? kLoRows * kLoStride : 0);  // (EXACT) their fp32 lo parts
+  float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sLoL + kLoRows * kLoStride);   // [4][8]
+  float* sO = reinterpret_cast<float*>(sQ);                 // [GM][128] scaled partial O (after the tiles)
   float* sML = reinterpret_cast<float*>(sRed + 4);          // [0, 8) max, [8, 16) sum, [16, 24) lse2
   float* sCorr = sML + 24;                                  // [8]
   int* sRescale = reinterpret_cast<int*>(sCorr + 8);
@@ -141,7 +157,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   for (int o = tid; o < kLoRows * HALF; o += blockDim.x) {     // tab_lo rows: [64 hi | 64 lo]
     const int rr = o / HALF, ii = o % HALF;
     *reinterpret_cast<float2*>(sLo + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + ii];
-    *reinterpret_cast<float2*>(sLoL + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + HALF + ii];
+    if (EXACT) *reinterpret_cast<float2*>(sLoL + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + HALF + ii];
   }
   for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
@@ -167,7 +183,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         if (j >= kKStages) tc::mbar_wait(kempty + s, ((j / kKStages) - 1) & 1);
         int start, len, pe0;
         tile_info(tbeg + j, start, len, pe0);
-        uint8_t* st = sK + s * kKStageBytes;
+        uint8_t* st = sK + s * kTileBytes32K;
         const int a0 = pe0 >> 5, nA = ((pe0 + len - 1) >> 5) - a0 + 1;
         const uint32_t bytes = (start < p.S_tot ? 32768u : 0u) + (uint32_t)nA * kRowBytes;
         tc::mbar_expect_tx(kfull + s, bytes);
@@ -176,7 +192,8 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
           for (int kb = 0; kb < 2; ++kb) tc::tma_load_2d(st + kb * 16384, &tm_k, kfull + s, kb * 64, row);
         }
         for (int r = 0; r < nA; ++r)
-          tc::bulk_load(st + 32768 + r * kRowBytes, p.tab_hi + (long long)(a0 + r) * 2 * HALF, kRowBytes, kfull + s);
+          tc::bulk_load(sA + s * Lay::kARows + r * kRowBytes, p.tab_hi + (long long)(a0 + r) * 2 * HALF, kRowBytes,
+                        kfull + s);
       }
     }
   } else if (warp == 3) {
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         if (j >= kVStages) tc::mbar_wait(vempty + s, ((j / kVStages) - 1) & 1);
         int start, len, pe0;
         tile_info(tbeg + j, start, len, pe0);
-        uint8_t* st = sV + s * kVStageBytes;
+        uint8_t* st = sV + s * kTileBytes32K;
         if (start < p.S_tot) {
           tc::mbar_expect_tx(vfull + s, 32768u);
           const int row = (int)((long long)bg * p.S_tot + start);
@@ -203,7 +220,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       const uint32_t aQ = tc::smem_u32(sQ), aP = tc::smem_u32(sP);
       auto qk = [&](int j) {
         const int s = j % kKStages;
-        const uint32_t st = tc::smem_u32(sK + s * kKStageBytes);
+        const uint32_t st = tc::smem_u32(sK + s * kTileBytes32K);
         tc::mbar_wait(rot_full + 2 * s, (j / kKStages) & 1);       // both rotated halves in place
         tc::mbar_wait(rot_full + 2 * s + 1, (j / kKStages) & 1);
         tc::tc_fence_after();
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       for (int j = 0; j < nt; ++j) {
         if (j + 1 < nt) qk(j + 1);                          // overlaps softmax(j)
         const int s = j % kVStages;
-        const uint32_t st = tc::smem_u32(sV + s * kVStageBytes);
+        const uint32_t st = tc::smem_u32(sV + s * kTileBytes32K);
         tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);       // P^T written (and O^T rescaled)
         tc::mbar_wait(vfull + s, (j / kVStages) & 1);
         tc::tc_fence_after();
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
     const int rwg = (tid - 256) >> 7;                        // chunks [4 rwg, 4 rwg + 4)
     for (int j = 0; j < nt; ++j) {
       const int s = j % kKStages;
-      uint8_t* st = sK + s * kKStageBytes;
+      uint8_t* st = sK + s * kTileBytes32K;
       int start, len, pe0;
       tile_info(tbeg + j, start, len, pe0);
       const bool valid = t < len;
@@ -256,7 +273,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         //      recomputed exactly as rope_prep does it: fp64 table, double products, double ->
         //      float -> bf16 (reading Q17).
         const int hr = (pe >> 5) - (pe0 >> 5);
-        const float2* hi = reinterpret_cast<const float2*>(st + 32768 + (valid ? hr : 0) * kRowBytes);
+        const float2* hi = reinterpret_cast<const float2*>(sA + s * Lay::kARows + (valid ? hr : 0) * kRowBytes);
         const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
         const float2* lo_l = reinterpret_cast<const float2*>(sLoL + (pe & 31) * kLoStride);
 #pragma unroll 1
@@ -292,7 +309,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
             const float2 y1l = __fadd2_rn(y1, nd), y1h = __fadd2_rn(y1, dl);
             const float2 y2l = __fadd2_rn(y2, nd), y2h = __fadd2_rn(y2, dl);
             uint32_t r1 = tc::pack_bf16(y1l.x, y1l.y), r2 = tc::pack_bf16(y2l.x, y2l.y);
-            if (valid && (r1 != tc::pack_bf16(y1h.x, y1h.y) || r2 != tc::pack_bf16(y2h.x, y2h.y))) {
+            if (EXACT && valid && (r1 != tc::pack_bf16(y1h.x, y1h.y) || r2 != tc::pack_bf16(y2h.x, y2h.y))) {
               // exact: cos / sin from the double-float tables (hi + lo) by angle addition in
               // double, then rope_prep's arithmetic (double products, double -> float -> bf16)
               float o1[2], o2[2];
@@ -321,7 +338,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         //      its V row goes to the V stage once that is free ----
         const int sv_i = j % kVStages;
         tc::mbar_wait(vfull + sv_i, (j / kVStages) & 1);
-        uint8_t* sv = sV + sv_i * kVStageBytes;
+        uint8_t* sv = sV + sv_i * kTileBytes32K;
         const int off_base = t * 128;
         for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
           const int off = off_base + ((c ^ (t & 7)) << 4);
@@ -690,12 +707,12 @@ size_t decode_nsplit(const DecodeParams& p) {
   return (size_t)best;            // 0: the cache is too large for the in-TMEM logits
 }
 
-template <int GM>
+template <int GM, bool EXACT>
 cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel, const int32_t* phase_begin_dev,
                          int32_t n_phase, __nv_bfloat16* out, const CUtensorMap& tk, const CUtensorMap& tv,
                          cudaStream_t st) {
-  const size_t smem = decode_fused_smem(GM);
-  auto kern = decode_fused_kernel<GM>;
+  const size_t smem = DecLayout<EXACT>::smem(GM);
+  auto kern = decode_fused_kernel<GM, EXACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -717,10 +734,14 @@ cudaError_t launch_decode_fused(const DecodeParams& p, const PlanDev& pl, int32_
                                 const int32_t* phase_begin_dev, int32_t n_phase, __nv_bfloat16* out,
                                 const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t st) {
   const int GM = decode_gm(p.G);
-  if (GM == 1) return launch_fused<1>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  if (GM == 2) return launch_fused<2>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  if (GM == 4) return launch_fused<4>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
-  return launch_fused<8>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  auto go = [&](auto exact) {
+    constexpr bool E = decltype(exact)::value;
+    if (GM == 1) return launch_fused<1, E>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+    if (GM == 2) return launch_fused<2, E>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+    if (GM == 4) return launch_fused<4, E>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+    return launch_fused<8, E>(p, pl, n_sel, phase_begin_dev, n_phase, out, tk, tv, st);
+  };
+  return p.exact_rope ? go(std::true_type{}) : go(std::false_type{});
 }
 
 cudaError_t launch_decode_commit(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,

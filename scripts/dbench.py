@@ -7,8 +7,9 @@ from paper_2406_17808_b200.synth import Synth
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+exact = len(sys.argv) > 3 and sys.argv[3] == "exact"
 cfg = C.CascadeConfig(batch=B, num_q_heads=32, num_kv_heads=8, head_dim=128, sink_size=64, cache_size=16384,
-                      num_cascades=4, max_stride=4096, dtype="bf16")
+                      num_cascades=4, max_stride=4096, dtype="bf16", exact_decode_rope=exact)
 cas = C.Cascade(cfg)
 syn = Synth(B, 32, 8, 128, seed=4)
 g = torch.Generator(device="cuda").manual_seed(4)
@@ -30,4 +31,4 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / (steps - 3)
 n_c = cas.state(0)["n_cached"]
 byt = B * 8 * (n_c + 1) * (4 * 128 + 20)   # K, V + mu r/w + s per key
-print(f"B={B} n_cached={n_c}: {ms:.3f} ms/step, {B / ms * 1e3:,.0f} tok/s, {byt / ms / 1e6:,.0f} GB/s algorithmic")
+print(f"{'exact' if exact else 'fast'} rope B={B} n_cached={n_c}: {ms:.3f} ms/step, {B / ms * 1e3:,.0f} tok/s, {byt / ms / 1e6:,.0f} GB/s algorithmic")

@@ -45,7 +45,8 @@ def test_gqa_groups_prefill_and_decode(Hq, d, reduce):
     kernels for G in {1, 2, 4, 8} at d = 128, the m = 1 strided path otherwise), B = 2, ragged
     strides, then 24 decode steps; outputs, exact masses and the cascade contents vs the oracle."""
     cfg = C.CascadeConfig(batch=2, num_q_heads=Hq, num_kv_heads=2, head_dim=d, sink_size=4, cache_size=96,
-                          num_cascades=3, max_stride=160, dtype="bf16", head_reduce=reduce)
+                          num_cascades=3, max_stride=160, dtype="bf16", head_reduce=reduce,
+                          exact_decode_rope=True)
     syn = Synth(2, Hq, 2, d, seed=300 + Hq + d)
     gpu, orc = C.Cascade(cfg), _orc(cfg)
     start = 0

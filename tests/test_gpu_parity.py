@@ -176,12 +176,31 @@ def test_cfg2_full_end_to_end_bf16():
     print(f"cfg2: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
 
 
+def assert_decode_masses(sg, s_ref, exact_rope):
+    """Decode masses vs the oracle.  exact_rope (CASCADE_OPT_EXACT_DECODE_ROPE): every entry within
+    S_RTOL.  Default fp32 key rotation: its bf16 rounding is one ulp off on ~2e-5 of the key
+    elements; a flip on a salient coordinate (|q_i| <= 2, |k_i| <= 64: <= 2 * 0.5 / sqrt(128) =
+    0.09 in the logit) moves that key's mass by <= ~10 %, so at most max(1, 1e-3 n) entries may
+    exceed S_RTOL and none may exceed 0.15."""
+    if exact_rope:
+        np.testing.assert_allclose(sg, s_ref, rtol=S_RTOL, atol=1e-30)
+        return
+    big = np.abs(s_ref) > 1e-30
+    rel = np.zeros_like(s_ref)
+    rel[big] = np.abs(sg[big] - s_ref[big]) / np.abs(s_ref[big])
+    assert np.abs(sg[~big]).max(initial=0.0) <= 1e-30
+    assert rel.max() <= 0.15, rel.max()
+    assert (rel > S_RTOL).sum() <= max(1, int(1e-3 * rel.size)), (rel > S_RTOL).sum()
+
+
+@pytest.mark.parametrize("exact_rope", [True, False])
 @pytest.mark.parametrize("Hq", [8, 6])
-def test_decode_matches_oracle(Hq):
-    """Eq. 2 steps after a short prefill, bf16, GQA 4:1 (the dedicated decode kernels) and 3:1
-    (a group size they are not instantiated for: the m = 1 strided path), B = 3."""
+def test_decode_matches_oracle(Hq, exact_rope):
+    """Eq. 2 steps after a short prefill, bf16, GQA 4:1 and 3:1 (the fused cluster decode kernel
+    at GM = 4), B = 3, with and without the proven-exact key rotation."""
     cfg = C.CascadeConfig(batch=3, num_q_heads=Hq, num_kv_heads=2, head_dim=128, sink_size=4,
-                          cache_size=64, num_cascades=4, max_stride=32, dtype="bf16")
+                          cache_size=64, num_cascades=4, max_stride=32, dtype="bf16",
+                          exact_decode_rope=exact_rope)
     syn = Synth(3, Hq, 2, 128, seed=77)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))
@@ -196,7 +215,7 @@ def test_decode_matches_oracle(Hq):
         O_ref, s_ref = orc.decode(0, _np(q[:, 0]), _np(k[:, 0]), _np(v[:, 0]))
         torch.cuda.synchronize()
         assert np.abs(_np(out) - O_ref).max() <= O_TOL["bf16"]
-        np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=S_RTOL, atol=1e-30)
+        assert_decode_masses(_np(gpu.last_scores(0)), s_ref, exact_rope)
     _compare_state(gpu.state(0), orc.state(0), exact_mu=False)
 
 
@@ -213,7 +232,8 @@ def test_ablation_variants_end_to_end(dtype, head_reduce, selection, head_policy
     d = 128 if dtype == "bf16" else 64
     cfg = C.CascadeConfig(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=d, sink_size=4,
                           cache_size=64, num_cascades=4, max_stride=48, dtype=dtype,
-                          head_reduce=head_reduce, selection=selection, head_policy=head_policy)
+                          head_reduce=head_reduce, selection=selection, head_policy=head_policy,
+                          exact_decode_rope=True)
     syn = Synth(2, 8, 2, d, seed=1234, dtype=cfg.torch_dtype)
     gpu = C.Cascade(cfg)
     orc = CascadeOracle(_oracle_cfg(cfg))
