@@ -33,6 +33,7 @@ struct LayerBufs {
   void* k_raw; void* v; double* mu; int64_t* origin; int32_t* pe;
   // per-call scratch (per layer so layers may run on different streams)
   float* s; float* lse; int32_t* plan; int32_t* resolved;
+  float* s_heads;           // one-pass mode: per-q-head estimated mass [B][Hq][S_tot + Mb]
   void* q_rot; void* k_rot; void* v_chunk;
   uint32_t* maint_ctl;      // [0] grid-barrier counter, then per-(b, g) 64-bit counts of rows
                             // actually rewritten (8-byte aligned)
@@ -72,7 +73,7 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 }
 
 struct Sizes {
-  size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk;
+  size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk, s_heads;
   size_t maint_ctl;
   size_t per_layer;
   size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
@@ -93,6 +94,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.pe = align_up(S * 4);
   z.s = align_up(B * Hk * (S + M) * 4);
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
+  z.s_heads = (c.options & CASCADE_OPT_ONEPASS_SCORES) ? align_up(B * Hq * (S + (M + 127) / 128 * 128) * 4) : 0;
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
@@ -104,7 +106,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.v_chunk = align_up(B * Hk * M * d * es);
   z.maint_ctl = align_up(8 + 8 * B * Hk);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl;
+                z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl + z.s_heads;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * d * sizeof(float2));   // [a][hi parts | lo parts]
   z.tab_lo = align_up(32 * d * sizeof(float2));
@@ -344,6 +346,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.pe = reinterpret_cast<int32_t*>(take(sz.pe));
     L.s = reinterpret_cast<float*>(take(sz.s));
     L.lse = reinterpret_cast<float*>(take(sz.lse));
+    L.s_heads = sz.s_heads ? reinterpret_cast<float*>(take(sz.s_heads)) : nullptr;
     L.plan = reinterpret_cast<int32_t*>(take(sz.plan));
     L.resolved = reinterpret_cast<int32_t*>(take(sz.resolved));
     L.q_rot = take(sz.q_rot); L.k_rot = take(sz.k_rot); L.v_chunk = take(sz.v_chunk);
@@ -691,8 +694,11 @@ cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, cons
     tp.mu = g.homogeneous ? nullptr : L.mu;   // pass 2 folds the EMA in its epilogue
     tp.decay = g.decay;
     tp.head_reduce = g.head_reduce;
+    tp.w = up.w;
+    tp.s_heads = L.s_heads;                   // non-null: the one-pass estimator (no pass 2)
     if (cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st) != cudaSuccess)
       return CASCADE_ERR_CUDA;
+    if (L.s_heads && cudaMemsetAsync(L.s_heads, 0, h->sz.s_heads, st) != cudaSuccess) return CASCADE_ERR_CUDA;
     ProfScope ps(h, 1, st);
     launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
     ps.finish(useful);
@@ -705,7 +711,12 @@ cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, cons
   if (!launches_ok()) return CASCADE_ERR_CUDA;   // nothing of the cascade state has changed yet
   // from here on a launch may mutate the cascade state (pass 2 folds mu in its epilogue)
   if constexpr (kTc) {
-    if (h->cfg.ema_gamma != 1.0) {
+    if (L.s_heads) {          // one-pass estimates: group reduction (+ the fold) in one pass
+      ProfScope ps(h, 2, st);
+      launch_onepass_reduce(tp, g, /*fold=*/!g.homogeneous, st);
+      ps.finish(0.0);
+      ++h->launches;
+    } else if (h->cfg.ema_gamma != 1.0) {
       ProfScope ps(h, 2, st);
       launch_attn_score_tc(tp, L.tm_q, L.tm_k, g.d, st);
       ps.finish(useful);

@@ -134,7 +134,13 @@ struct TcParams {
   double* mu;                   // [B*Hkv][S_tot] EMA state: pass 2 folds mu <- decay*mu + s
   double decay;                 // gamma^m
   int32_t head_reduce;          // s_g over the group: 0 max; ablations 1 mean, 2 median
+  // one-pass estimator (CASCADE_OPT_ONEPASS_SCORES): pass 1 accumulates every q-head's estimated
+  // mass (Alg. 3) into s_heads [B][Hq][S_tot + Mb] (zeroed per call, atomic adds)
+  const float* w;               // [m] EMA row weights (1 - gamma) gamma^(m-1-r)
+  float* s_heads;               // null: exact mode (pass 2)
 };
+// per-key group reduction + EMA fold of the one-pass estimates (k_attn_tc.cu)
+void launch_onepass_reduce(const TcParams& p, const Geometry& g, bool fold, cudaStream_t st);
 // single-token decode (k_decode.cu): one fused cluster launch per step
 struct DecodeParams {
   int32_t B, Hq, Hkv, G, S_tot, alpha, N, c;
@@ -174,7 +180,7 @@ cudaError_t launch_decode_fused(const DecodeParams& p, const PlanDev& pl, int32_
 cudaError_t launch_decode_commit(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
                                  const int32_t* phase_begin_dev, int32_t n_phase, cudaStream_t st);
 
-size_t attn_fwd_tc_smem(int d);
+size_t attn_fwd_tc_smem(int d, bool est);
 
 size_t attn_score_tc_smem(int d, int G);
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -50,26 +50,39 @@ __device__ unsigned long long* g_p1_trace = nullptr;
 // O [256, 256+D), Q [384, 384+D/2); P of tile j (bf16 pairs) overwrites the upper half of S_(j%2).
 // MMA issue order QK(0) QK(1) PV(0) QK(2) PV(1) ...; tcgen05.mma from one thread execute in
 // order, so QK(j+2) overwrites S_(j%2) only after PV(j) has read P(j) from it.
-template <int D, int EMU>
+// EST (CASCADE_OPT_ONEPASS_SCORES): the paper's one-pass estimate of the per-key mass (Alg. 3,
+// P:628-650) inside pass 1, so no pass 2 runs.  After tile j's softmax, row r's weight is
+// a_r = C_EMA[r] / (l_r + l_r rho / gamma_) with gamma_ = j + 1 steps done and rho = nt - j - 1 left
+// (l_r and P share the running max, so P / l_r is the max-independent ratio the paper
+// normalises).  The column sum over the 128 rows, sum_r a_r P[r, key], is one more MMA: P (bf16,
+// also written to shared memory in the SWIZZLE_128B row layout) read as the MN-major A operand
+// [keys x rows] times B = [rows x 16] holding a_r split into bf16 hi + lo columns, into a 16-column
+// TMEM accumulator (double-buffered); the softmax warps read tile j-1's column sums while tile j's
+// MMAs run and atomically add them to s_heads.  K/V use a 2-stage ring to make room for the two
+// P buffers (64 KB).
+template <int D, int EMU, bool EST>
 __global__ void __launch_bounds__(256, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_vs, const __grid_constant__ CUtensorMap tm_vc,
                    TcParams p) {
   constexpr int KB = D / 64;                   // 64-element K blocks of a row
-  constexpr int kStages = 3;
-  constexpr uint32_t kColO = 256, kColQ = 384;
+  constexpr int kStages = EST ? 2 : 3;
+  constexpr uint32_t kColO = 256, kColQ = 384, kColCs = 448;   // EST: column sums at 448 / 464
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;                                   // kStages x KB blocks
   uint8_t* sV = sK + kStages * KB * kTileBytes;         // kStages x KB blocks
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * KB * kTileBytes);
+  uint8_t* sPb = sV + kStages * KB * kTileBytes;        // EST: 2 x P [128 rows x 128 keys] SW128 (2 blocks)
+  uint8_t* sB2 = sPb + (EST ? 2 * 2 * kTileBytes : 0);  // EST: 2 x [16 x 128] K-major SW128 (2 KB blocks)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB2 + (EST ? 2 * 4096 : 0));
   uint64_t* kv_full = bars + 0;      // [3]
   uint64_t* kv_empty = bars + 3;     // [3]
   uint64_t* s_full = bars + 6;       // [2]
   uint64_t* p_full = bars + 8;       // [2]
   uint64_t* q_full = bars + 10;
   uint64_t* pv_done = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* cs_done = bars + 12;     // [2] EST: column sums of tile j in TMEM buffer j % 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -84,7 +97,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
     tc::mbar_init(q_full, 4);
     tc::mbar_init(pv_done, 1);
+    tc::mbar_init(cs_done + 0, 1);
+    tc::mbar_init(cs_done + 1, 1);
     tc::fence_mbar_init();
+  }
+  if (EST) {                                            // B operand rows 2..15 stay zero
+    for (int o = threadIdx.x; o < 2 * 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sB2)[o] = make_uint4(0u, 0u, 0u, 0u);
+    tc::fence_proxy_async_smem();
   }
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_vs); tc::tma_prefetch(&tm_vc);
@@ -165,6 +184,18 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         }
         tc::mma_commit(kv_empty + (j % kStages));
         tc::mma_commit(pv_done);
+        if (EST) {                                      // column sums sum_r a_r P[r, key]
+          constexpr uint32_t idesc_cs = tc::idesc_bf16_f32(128, 16, 0, 1);   // A MN-major, B K-major
+          const uint32_t pb = tc::smem_u32(sPb) + (j & 1) * 2 * kTileBytes;
+          const uint32_t bb = tc::smem_u32(sB2) + (j & 1) * 4096;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {             // 128 rows = 8 x K16
+            const uint64_t da = tc::desc_mnmajor_sw128(pb + kk * 2048, kTileBytes);
+            const uint64_t db = tc::desc_kmajor_sw128(bb + (kk >> 2) * 2048 + (kk & 3) * 32);
+            tc::mma_bf16_ss(tmem + kColCs + (j & 1) * 16, da, db, idesc_cs, kk > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(cs_done + (j & 1));
+        }
       };
       tc::mbar_wait(q_full, 0);
       tc::tc_fence_after();
@@ -209,6 +240,24 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     }
     float m_used = -INFINITY, l = 0.f;
     float x[128];
+    // EST: tile jj's column sums (lane = key) -> s_heads[b][h][key] (atomic: every q-tile adds)
+    auto est_readout = [&](int jj) {
+      tc::mbar_wait(cs_done + (jj & 1), (jj >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t cv[2];
+      tc::tmem_ld_n<2>(tmem + kColCs + (jj & 1) * 16 + lane_off, cv);
+      tc::tmem_wait_ld();
+      const float v = __uint_as_float(cv[0]) + __uint_as_float(cv[1]);
+      int key, len;
+      if (jj < p.n_res_tiles) {
+        const int2 t2 = p.res_tiles[jj];
+        key = t2.x + r; len = t2.y;
+      } else {
+        const int k0 = (jj - p.n_res_tiles) * 128;
+        key = p.S_tot + k0 + r; len = min(128, p.m - k0);
+      }
+      if (r < len && v != 0.f) atomicAdd(p.s_heads + ((long long)b * p.Hq + h) * (p.S_tot + p.Mb) + key, v);
+    };
 #ifdef CASCADE_PASS1_TRACE
     long long w_s = 0, w_pv = 0;
 #endif
@@ -257,6 +306,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             pk[e] = tc::pack_bf16(pp.x, pp.y);
           }
           tc::tmem_st16(sb + 64 + c * 16, pk);
+          if (EST) {                                      // the same bf16 P, row r, keys [32c, 32c + 32)
+            uint8_t* prow = sPb + (j & 1) * 2 * kTileBytes + (c >> 1) * kTileBytes + r * 128;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int ch = ((c & 1) * 4 + q4) ^ (r & 7);
+              *reinterpret_cast<uint4*>(prow + ch * 16) =
+                  make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            }
+          }
         }
         if (decltype(track)::value) mraw = fmaxf(m0, m1);
         const float2 s01 = __fadd2_rn(s0, s1);
@@ -307,11 +365,25 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
           l += sum;
         }
       }
+      if (EST) {
+        // a_r = C_EMA[r] / (l_r (1 + rho / gamma_)) = C_EMA[r] (j + 1) / (nt l_r), split into
+        // bf16 hi + lo as columns 0 and 1 of the column-sum MMA's B operand (row r = K index r)
+        const float a = (qi < p.m && l > 0.f) ? p.w[qi] * (float)(j + 1) / ((float)nt * l) : 0.f;
+        const __nv_bfloat16 ah = __float2bfloat16_rn(a);
+        const __nv_bfloat16 al = __float2bfloat16_rn(a - __bfloat162float(ah));
+        uint8_t* b2 = sB2 + (j & 1) * 4096 + (r >> 6) * 2048;
+        const int kc = (r & 63) >> 3, ke = (r & 7) * 2;
+        *reinterpret_cast<__nv_bfloat16*>(b2 + 0 * 128 + ((kc ^ 0) << 4) + ke) = ah;
+        *reinterpret_cast<__nv_bfloat16*>(b2 + 1 * 128 + ((kc ^ 1) << 4) + ke) = al;
+        tc::fence_proxy_async_smem();
+      }
       tc::tmem_wait_st();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
+      if (EST && j > 0) est_readout(j - 1);
     }
+    if (EST && nt > 0) est_readout(nt - 1);
     // epilogue.  pv_done completes once per PV; when the last P is written only PV(nt-3) is
     // known complete (QK(nt-1) followed it), so a parity wait for phase nt-1 alone could be
     // satisfied by phase nt-3: wait for nt-2 first, then nt-1.
@@ -579,9 +651,10 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   }
 }
 
-size_t attn_fwd_tc_smem(int d) {
+size_t attn_fwd_tc_smem(int d, bool est) {
   const int KB = d / 64;
-  return 1024 + (size_t)(2 * 3 * KB) * kTileBytes + 16 * 8 + 64;
+  return est ? 1024 + (size_t)(2 * 2 * KB) * kTileBytes + 2 * 2 * kTileBytes + 2 * 4096 + 16 * 8 + 64
+             : 1024 + (size_t)(2 * 3 * KB) * kTileBytes + 16 * 8 + 64;
 }
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
@@ -592,7 +665,8 @@ size_t attn_score_tc_smem(int d, int G) {
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                         const CUtensorMap& tvs, const CUtensorMap& tvc, int d, cudaStream_t st) {
   dim3 grid((p.m + 127) / 128, p.Hq, p.B);
-  const size_t smem = attn_fwd_tc_smem(d);
+  const bool est = p.s_heads != nullptr;
+  const size_t smem = attn_fwd_tc_smem(d, est);
   // 4 of every 16 exp2 pairs on the FMA pipe: measured 75.1 / 78.3 / 78.4 / 76.0 % of peak for
   // 0 / 4 / 6 / 8 (scripts/kbench.py, steady state n_c = 62.5K)
   auto go = [&](auto kern) {
@@ -608,8 +682,13 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
     cudaMemcpyToSymbol(g_p1_trace, &trace, sizeof(trace));
   }
 #endif
-  if (d == 128) go(attn_fwd_tc_kernel<128, 4>);
-  else go(attn_fwd_tc_kernel<64, 4>);
+  if (est) {
+    if (d == 128) go(attn_fwd_tc_kernel<128, 4, true>);
+    else go(attn_fwd_tc_kernel<64, 4, true>);
+  } else {
+    if (d == 128) go(attn_fwd_tc_kernel<128, 4, false>);
+    else go(attn_fwd_tc_kernel<64, 4, false>);
+  }
 #ifdef CASCADE_PASS1_TRACE
   if (++calls % 16 == 0 && ctas <= 4096LL * 64) {
     std::vector<unsigned long long> h(ctas * 6);
@@ -642,6 +721,39 @@ void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtens
   } else {
     go(attn_score_tc_kernel<64, 4, 3>);
   }
+}
+
+// One-pass mode, after pass 1: s_g[key] = reduce_h s_heads[b][g G + h][key] over the group (max,
+// P:542; mean / median ablations), and the EMA fold of the residents (mu <- decay mu + s_g, never
+// an FMA) unless the homogeneous policy folds later.  One thread per (b, g, key) of the slot
+// space [0, S_tot + m); empty slots keep s = 0.
+__global__ void onepass_reduce_kernel(TcParams p, int32_t sink_pre, Geometry g, bool fold) {
+  const long long total = (long long)p.B * p.Hkv * (p.S_tot + p.m);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long bg = i / (p.S_tot + p.m);
+    const int x = (int)(i - bg * (p.S_tot + p.m));
+    const int b = (int)(bg / p.Hkv), gg = (int)(bg - (long long)b * p.Hkv);
+    bool valid = x >= p.S_tot || slot_pe(g, x) >= 0;
+    if (!valid) continue;
+    float hv[kMaxMedianGroup];
+    float best = 0.f;
+    for (int hh = 0; hh < p.G; ++hh) {
+      const float v = p.s_heads[((long long)b * p.Hq + gg * p.G + hh) * (p.S_tot + p.Mb) + x];
+      if (hh < kMaxMedianGroup) hv[hh] = v;
+      best = fmaxf(best, v);
+    }
+    if (p.head_reduce) best = group_reduce_ablation(hv, p.G, p.head_reduce);
+    p.s[bg * (p.S_tot + p.m) + x] = best;
+    if (fold && x < p.S_tot)
+      p.mu[bg * p.S_tot + x] = __dadd_rn(__dmul_rn(p.decay, p.mu[bg * p.S_tot + x]), (double)best);
+  }
+}
+
+void launch_onepass_reduce(const TcParams& p, const Geometry& g, bool fold, cudaStream_t st) {
+  const long long total = (long long)p.B * p.Hkv * (p.S_tot + p.m);
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+  onepass_reduce_kernel<<<blocks, 256, 0, st>>>(p, g.sink_pre, g, fold);
 }
 
 }  // namespace cascade
