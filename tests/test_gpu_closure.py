@@ -168,8 +168,9 @@ def test_onepass_estimator_matches_its_tile_order_oracle(reduce):
         np.testing.assert_allclose(_np(gpu.last_scores(0)), s_ref, rtol=5e-3, atol=1e-30)
         _contents_equal(gpu.state(0), orc.state(0))
         _, s_ex = exact.prefill_stride(0, _np(q), _np(k), _np(v))
-        big = s_ex > 1e-12
-        worst = max(worst, float(np.max(np.abs(s_ref[big] - s_ex[big]) / s_ex[big])))
+        if start <= 64 + 2 * 256:          # no token dropped yet: both oracles hold the same cache
+            big = s_ex > 1e-12
+            worst = max(worst, float(np.max(np.abs(s_ref[big] - s_ex[big]) / s_ex[big])))
     margins = orc.select_margins()
     assert margins.size > 0 and margins.min() > 5e-3, margins.min()
     print(f"one-pass estimate vs exact mass: max relative deviation {worst:.3f}")
