@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--streams", type=int, default=0, help="concurrent layer streams (default min(L, 4))")
     ap.add_argument("--shard-of", type=int, default=1, help="N = 1: run rank 0's shard of a W-rank job")
     ap.add_argument("--tokens", type=int, default=0, help="override sequence length (debug only)")
+    ap.add_argument("--score-mode", default="exact", choices=["exact", "onepass"],
+                    help="per-key mass: exact two-pass (default) or the paper's one-pass estimator")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -357,7 +359,7 @@ def main():
     cfg = C.CascadeConfig(num_layers=L, batch=B, num_q_heads=hq, num_kv_heads=hk, head_dim=d,
                           sink_size=spec["sink_size"], cache_size=spec["cache_size"],
                           num_cascades=spec["num_cascades"], max_stride=m, dtype="bf16",
-                          rope_theta=spec["rope_theta"])
+                          rope_theta=spec["rope_theta"], score_mode=args.score_mode)
     cas = C.Cascade(cfg, device=local)
 
     # ---- inputs, generated on the device (full heads, then this rank's shard), per layer seed ----
@@ -509,7 +511,7 @@ def main():
                          "cache": spec["cache_size"], "sinks": spec["sink_size"],
                          "cascades": spec["num_cascades"], "heads": f"{Hq}q/{Hk}kv d={d}",
                          "heads_per_rank": f"{hq}q/{hk}kv", "layers": L, "layer_streams": S,
-                         "distinct_input_sets": n_sets, "parallelism": par,
+                         "distinct_input_sets": n_sets, "parallelism": par, "score_mode": args.score_mode,
                          "l2": "inputs and cache state exceed L2; no flush needed"},
               "roofline": roof, "roofline_other": extra_roof, "kernels": kern, "kernel_share": share,
               "gpu_launches": launches, "clocks": clk}

@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   uint64_t* s_full = bars + 12;     // [2] per S^T buffer
   uint64_t* p_full = bars + 14;     // [2] per S^T buffer
   uint64_t* pv_done = bars + 16;
-  uint64_t* vfull = bars + 17;      // [2]
-  uint64_t* vempty = bars + 19;     // [2]
+  uint64_t* vfull = bars + 17;      // [kVStages <= 3]
+  uint64_t* vempty = bars + 20;     // [kVStages <= 3]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int split = blockIdx.x, bg = blockIdx.y;
