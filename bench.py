@@ -69,6 +69,10 @@ WORKLOADS = {
                  "synthetic prefill through a 65K cascade cache (64 sinks + 8 x 8192), stride 4096"),
     "cfg2": dict(name="cfg2_llama8b_4k", desc="configs[1]: Llama-3-8B attention layer, 32K prefill, "
                  "4K cascade cache (64 sinks + 4 x 1024), stride 1024"),
+    "stack": dict(name="cfg5_8gpu_32l", desc="SURVEY 8(f) NEXT #4: coupled Llama-3-8B attention layers (d_model 4096, "
+                  "synthetic q/k/v/o projections + residual, layer l+1 fed by layer l), 1M-token prefill through a "
+                  "65K cascade cache per layer (64 sinks + 8 x 8192), stride 4096, layers as a wavefront over "
+                  "per-layer streams"),
     "cfg5": dict(name="cfg5_8gpu_32l", desc="configs[4]: 32 independent Llama-3-8B attention layers, 1M-token "
                  "passkey-shaped synthetic prefill through a 65K cascade cache each (64 sinks + 8 x 8192), "
                  "stride 4096, head-sharded across the ranks"),
@@ -303,6 +307,83 @@ def decode_bench(args, dev, spec, peaks, world, rank, comm, use_dist):
     return res
 
 
+def stack_bench(args, spec, wl, peaks):
+    """--workload stack: Alg. 1's layer loop over L coupled synthetic attention
+    layers through cascade_stack_prefill (projections by cuBLASLt inside the library, every layer's
+    attention + cache update by the cascade kernels, the layers of consecutive chunks overlapping on
+    per-layer streams).  One step = the whole sequence through every layer from empty caches."""
+    import torch
+    from paper_2406_17808_b200 import cascade as C
+    L = args.layers or 4
+    Hq, Hk, d, m, T, B = (spec["num_q_heads"], spec["num_kv_heads"], spec["head_dim"], spec["stride"],
+                          spec["tokens"], spec["batch"])
+    D = Hq * d
+    cfg = C.CascadeConfig(num_layers=L, batch=B, num_q_heads=Hq, num_kv_heads=Hk, head_dim=d,
+                          sink_size=spec["sink_size"], cache_size=spec["cache_size"],
+                          num_cascades=spec["num_cascades"], max_stride=m, dtype="bf16",
+                          rope_theta=spec["rope_theta"])
+    cas = C.Cascade(cfg)
+    g = torch.Generator(device="cuda").manual_seed(5_000_000)
+    sc = 1.0 / D ** 0.5
+    rnd = lambda *shape: (torch.randn(shape, generator=g, device="cuda") * sc).to(torch.bfloat16)
+    ws = [(rnd(D, Hq * d), rnd(D, Hk * d), rnd(D, Hk * d), rnd(Hq * d, D)) for _ in range(L)]
+    st = C.Stack(cas, ws, D)
+    x = torch.randn((B, T, D), generator=g, device="cuda").to(torch.bfloat16)
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    log(f"stack: {L} layers, inputs ready")
+
+    def step():
+        for l in range(L):
+            cas.reset(l)
+        st.prefill(x, m, y)
+
+    for i in range(args.warmup):
+        step()
+        torch.cuda.synchronize()
+        log(f"warmup step {i} done")
+    clocks = ClockSampler(0)
+    clocks.start()
+    cas.profile_enable(True)
+    cas.profile_read()
+    n0 = cas.launch_count()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = cas.profile_read()
+    clk = clocks.stop()
+    ms_step = ms / args.steps
+    useful = prof["attn_fwd"][2] / args.steps
+    nchunks = (T + m - 1) // m
+    gemm_flops = 2.0 * B * T * D * (Hq * d + 2 * Hk * d + Hq * d) * L
+    serial = sum(v[0] for v in prof.values()) / args.steps
+    res = {"metric": METRIC, "value": T * B / (ms_step / 1e3), "unit": "tok/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init projections)",
+           "config": {"workload": wl["desc"], "tokens": T, "batch": B, "stride": m, "layers": L, "d_model": D,
+                      "heads": f"{Hq}q/{Hk}kv d={d}", "cache": spec["cache_size"], "cascades": spec["num_cascades"],
+                      "l2": "inputs and cache state exceed L2; no flush needed"},
+           "stack": {"attention_useful_tflops": useful / (ms_step / 1e3) / 1e12,
+                     "gemm_tflops_per_step": gemm_flops / 1e12,
+                     "all_useful_tflops": (useful + gemm_flops) / (ms_step / 1e3) / 1e12,
+                     "peak_sustained": peaks["bf16_sus"],
+                     "cascade_kernels_ms_per_step": serial,
+                     "note": "cascade_kernels_ms_per_step sums the event-timed cascade launch groups of all layer "
+                             "streams (they overlap on the device, so it may exceed ms_per_step); the rest of the "
+                             "step is the cuBLASLt projections"},
+           "kernels": {k: {"ms_per_step": v[0] / args.steps, "launch_groups": v[1]} for k, v in prof.items() if v[1]},
+           "gpu_launches": cas.launch_count() - n0, "gpu_launches_note": "cascade kernels only (+ 4 cuBLASLt GEMMs "
+           f"per layer-chunk: {4 * L * nchunks * args.steps})", "clocks": clk}
+    print(json.dumps(res), flush=True)
+    st.close()
+    cas.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,6 +411,12 @@ def main():
     L = args.layers or spec["num_layers"]
     if args.impl == "reference":
         run_reference(args, spec, wl, L)
+        return
+    if args.workload == "stack":
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        if int(os.environ.get("RANK", "0")) == 0:
+            stack_bench(args, spec, wl, load_peaks())
         return
 
     import torch

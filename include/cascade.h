@@ -255,6 +255,70 @@ cascade_status cascade_commit(cascade_handle* h, int32_t layer, const void* k, c
 cascade_status cascade_load_state(cascade_handle* h, int32_t layer, const cascade_state_view* src,
                                   void* stream);
 
+/* Copies the handle's configuration into *out (host only). */
+cascade_status cascade_get_config(const cascade_handle* h, cascade_config* out);
+
+/* ---- coupled layer stack: Alg. 1's layer loop ------
+ *
+ * Alg. 1 runs, for every chunk, every layer of the model in order:
+ * layer l+1 consumes layer l's output of the same chunk, and layer l of the next
+ * chunk needs only layer l's cascade and layer l-1's output of that chunk.  A
+ * cascade_stack drives the L layers of a handle as synthetic attention layers
+ * with their projections and residual (the paper's model layers are trained
+ * blocks, out of scope):
+ *     q = x W_q, k = x W_k, v = x W_v   (plain library GEMMs, cuBLASLt, bf16 in /
+ *                                         out, fp32 accumulation)
+ *     out = cascade_prefill_stride(layer l, q, k, v)
+ *     x  <- x + out W_o                   (cuBLASLt, residual as the C operand)
+ * Each layer runs on its own stream; events order (chunk c, layer l) after (c,
+ * l-1) and after layer l+1 has finished reading the residual buffer it
+ * overwrites, so layer l of chunk c+1 runs while layer l+1 of chunk c does (the
+ * wavefront).  bf16 handles only (else UNSUPPORTED); head_dim, heads, batch,
+ * max_stride are the handle's; d_model D is free (the projections are D x H d). */
+typedef struct cascade_stack cascade_stack;
+
+typedef struct {
+  const void* w_q;  /* [D, Hq*d]  row-major bf16, device                         */
+  const void* w_k;  /* [D, Hkv*d]                                                */
+  const void* w_v;  /* [D, Hkv*d]                                                */
+  const void* w_o;  /* [Hq*d, D]                                                 */
+} cascade_layer_weights;
+
+/* Device bytes of a stack's workspace: per layer q/k/v/out scratch of max_stride
+ * rows, two residual-stream buffers [B, max_stride, D] per layer boundary (L+1),
+ * and a cuBLASLt workspace per layer stream.  0 if cfg is invalid or d_model < 1. */
+size_t cascade_stack_workspace_bytes(const cascade_config* cfg, int32_t d_model);
+
+/* Binds a stack to handle h (which it drives; do not call h's layers directly
+ * while a stack call is in flight).  w: num_layers weight sets (device pointers
+ * the caller keeps valid).  d_ws: caller-owned device workspace of at least
+ * cascade_stack_workspace_bytes, 256-B aligned.  Creates L streams, events and a
+ * cuBLASLt handle (host objects owned by the stack). */
+cascade_status cascade_stack_init(cascade_handle* h, int32_t d_model, const cascade_layer_weights* w,
+                                  void* d_ws, size_t ws_bytes, cascade_stack** out);
+
+void cascade_stack_destroy(cascade_stack* s);
+
+/* Strided prefill (Alg. 1) of a whole input through every layer:
+ *   x [B, T, D] bf16 (device or pinned host)  -- the stream of layer-0 inputs
+ *   y [B, T, D] bf16 (device or pinned host)  -- the last layer's residual stream
+ * in ceil(T/m) chunks of m <= max_stride tokens (the last may be ragged).  All work
+ * is enqueued before returning; `stream` waits for the last chunk's last layer
+ * (which orders every layer's work of the call).  Each chunk advances every
+ * layer's cascade by its length. */
+cascade_status cascade_stack_prefill(cascade_stack* s, const void* x, int64_t T, int32_t m, void* y,
+                                     void* stream);
+
+/* Test hook: after a cascade_stack_prefill and a synchronisation, device pointers to
+ * the per-layer intermediates of the LAST chunk processed (m_last rows each):
+ * x_in [B,m,D] (the layer's input), q [B,m,Hq,d], k/v [B,m,Hkv,d], o [B,m,Hq,d],
+ * x_out [B,m,D] (input + o W_o). */
+typedef struct {
+  int32_t m_last;
+  void *x_in, *q, *k, *v, *o, *x_out;
+} cascade_stack_view;
+cascade_status cascade_stack_trace(cascade_stack* s, int32_t layer, cascade_stack_view* out);
+
 /* ---- test hooks -------------------------------------------------------- */
 
 /* Score injection: fold the given per-key mass and insert the m tokens, with

@@ -65,7 +65,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     objs = [o for o, _ in results]
     changed = any(c for _, c in results)
     if changed or force or not os.path.exists(LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lcublasLt",
+               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

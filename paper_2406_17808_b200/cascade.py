@@ -59,6 +59,17 @@ class _StateView(ctypes.Structure):
                 ("origin", ctypes.c_void_p), ("pe", ctypes.c_void_p)]
 
 
+class _LayerWeights(ctypes.Structure):
+    _fields_ = [("w_q", ctypes.c_void_p), ("w_k", ctypes.c_void_p), ("w_v", ctypes.c_void_p),
+                ("w_o", ctypes.c_void_p)]
+
+
+class _StackView(ctypes.Structure):
+    _fields_ = [("m_last", ctypes.c_int32), ("x_in", ctypes.c_void_p), ("q", ctypes.c_void_p),
+                ("k", ctypes.c_void_p), ("v", ctypes.c_void_p), ("o", ctypes.c_void_p),
+                ("x_out", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -93,6 +104,13 @@ def lib():
             "cascade_score_buffer": (i32, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(i32)]),
             "cascade_commit": (i32, [vp, i32, vp, vp, vp]),
             "cascade_load_state": (i32, [vp, i32, ctypes.POINTER(_StateView), vp]),
+            "cascade_get_config": (i32, [vp, cfgp]),
+            "cascade_stack_workspace_bytes": (ctypes.c_size_t, [cfgp, i32]),
+            "cascade_stack_init": (i32, [vp, i32, ctypes.POINTER(_LayerWeights), vp, ctypes.c_size_t,
+                                         ctypes.POINTER(vp)]),
+            "cascade_stack_destroy": (None, [vp]),
+            "cascade_stack_prefill": (i32, [vp, vp, ctypes.c_int64, i32, vp, vp]),
+            "cascade_stack_trace": (i32, [vp, i32, ctypes.POINTER(_StackView)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -109,7 +127,8 @@ EXPORTED = ["cascade_status_string", "cascade_validate_config", "cascade_workspa
             "cascade_update_with_scores", "cascade_last_scores", "cascade_mirror_advance",
             "cascade_launch_count", "cascade_reset", "cascade_profile_enable",
             "cascade_profile_read", "cascade_attend", "cascade_score_buffer", "cascade_commit",
-            "cascade_load_state"]
+            "cascade_load_state", "cascade_get_config", "cascade_stack_workspace_bytes", "cascade_stack_init",
+            "cascade_stack_destroy", "cascade_stack_prefill", "cascade_stack_trace"]
 
 
 @dataclass
@@ -406,3 +425,78 @@ class Cascade:
                                           cnt.ctypes.data_as(ctypes.c_void_p),
                                           work.ctypes.data_as(ctypes.c_void_p)), "cascade_profile_read")
         return {n: (float(ms[i]), int(cnt[i]), float(work[i])) for i, n in enumerate(self.PROFILE_CLASSES)}
+
+
+class Stack:
+    """A cascade_stack (include/cascade.h): Alg. 1's layer loop over the handle's L layers as
+    synthetic attention layers (projections by cuBLASLt inside the library, attention and the cache
+    update by the cascade kernels), driven as a wavefront over per-layer library streams.
+
+    weights: L tuples (w_q [D, Hq d], w_k [D, Hkv d], w_v [D, Hkv d], w_o [Hq d, D]) of contiguous
+    bf16 device tensors, kept alive by this object."""
+
+    def __init__(self, cas: Cascade, weights, d_model: int):
+        c = cas.cfg
+        if c.dtype != "bf16":
+            raise ValueError("the stack runs bf16 handles")
+        if len(weights) != c.num_layers:
+            raise ValueError("one weight set per layer")
+        D, Hq, Hk, d = d_model, c.num_q_heads, c.num_kv_heads, c.head_dim
+        shapes = ((D, Hq * d), (D, Hk * d), (D, Hk * d), (Hq * d, D))
+        for l, ws in enumerate(weights):
+            for name, t, shp in zip(("w_q", "w_k", "w_v", "w_o"), ws, shapes):
+                if tuple(t.shape) != shp or t.dtype != torch.bfloat16 or not t.is_contiguous() \
+                        or t.device != cas.device:
+                    raise ValueError(f"layer {l} {name}: needs a contiguous bf16 {shp} tensor on {cas.device}")
+        self.cas, self.D, self.weights = cas, D, [tuple(w) for w in weights]
+        arr = (_LayerWeights * c.num_layers)(*[_LayerWeights(*(t.data_ptr() for t in ws)) for ws in self.weights])
+        L = lib()
+        nbytes = int(L.cascade_stack_workspace_bytes(ctypes.byref(c.c_struct()), D))
+        if nbytes == 0:
+            raise ValueError("invalid stack configuration")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=cas.device)
+        base = self.workspace.data_ptr()
+        self._s = ctypes.c_void_p()
+        _check(L.cascade_stack_init(cas._h, D, arr, ctypes.c_void_p(base + (-base) % 256), nbytes,
+                                    ctypes.byref(self._s)), "cascade_stack_init")
+
+    def close(self):
+        if self._s:
+            lib().cascade_stack_destroy(self._s)
+            self._s = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, x: torch.Tensor, m: int, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """x [B, T, D] bf16 (device, or pinned host) -> y [B, T, D] (same placement as given)."""
+        c = self.cas.cfg
+        if x.dim() != 3 or x.shape[0] != c.batch or x.shape[2] != self.D or x.dtype != torch.bfloat16 \
+                or not x.is_contiguous():
+            raise ValueError(f"x: needs a contiguous bf16 [{c.batch}, T, {self.D}] tensor")
+        if y is None:
+            y = torch.empty_like(x)
+        if tuple(y.shape) != tuple(x.shape) or y.dtype != x.dtype or not y.is_contiguous():
+            raise ValueError("y: needs x's shape and dtype")
+        for name, t in (("x", x), ("y", y)):
+            if t.is_cuda and t.device != self.cas.device:
+                raise ValueError(f"{name}: on {t.device}, the stack is on {self.cas.device}")
+            if not t.is_cuda and not t.is_pinned():
+                raise ValueError(f"{name}: host tensors must be pinned")
+        _check(lib().cascade_stack_prefill(self._s, _ptr(x), x.shape[1], m, _ptr(y), _stream(stream)),
+               "cascade_stack_prefill")
+        return y
+
+    def trace(self, layer: int) -> dict:
+        """The last chunk's intermediates of one layer (copies): x_in, q, k, v, o, x_out."""
+        sv = _StackView()
+        _check(lib().cascade_stack_trace(self._s, layer, ctypes.byref(sv)), "cascade_stack_trace")
+        c, m = self.cas.cfg, sv.m_last
+        B, Hq, Hk, d, D = c.batch, c.num_q_heads, c.num_kv_heads, c.head_dim, self.D
+        shp = dict(x_in=(B, m, D), q=(B, m, Hq, d), k=(B, m, Hk, d), v=(B, m, Hk, d), o=(B, m, Hq, d),
+                   x_out=(B, m, D))
+        return {n: torch.as_tensor(_DevArray(getattr(sv, n), s, "<i2"), device=self.cas.device).clone()
+                .view(torch.bfloat16) for n, s in shp.items()}

@@ -1139,6 +1139,12 @@ cascade_status cascade_load_state(cascade_handle* h, int32_t layer, const cascad
   return CASCADE_OK;
 }
 
+cascade_status cascade_get_config(const cascade_handle* h, cascade_config* out) {
+  if (!h || !out) return CASCADE_ERR_INVALID_ARG;
+  *out = h->cfg;
+  return CASCADE_OK;
+}
+
 cascade_status cascade_state(cascade_handle* h, int32_t layer, cascade_state_view* out, void* stream) {
   if (!h || !out || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
   if (h->poisoned) return CASCADE_ERR_POISONED;

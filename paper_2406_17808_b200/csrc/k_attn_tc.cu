@@ -82,7 +82,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   uint64_t* q_full = bars + 10;
   uint64_t* pv_done = bars + 11;
   uint64_t* cs_done = bars + 12;     // [2] EST: column sums of tile j in TMEM buffer j % 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* o_done = bars + 14;      // every MMA of the CTA complete (O final)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -99,6 +100,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     tc::mbar_init(pv_done, 1);
     tc::mbar_init(cs_done + 0, 1);
     tc::mbar_init(cs_done + 1, 1);
+    tc::mbar_init(o_done, 1);
     tc::fence_mbar_init();
   }
   if (EST) {                                            // B operand rows 2..15 stay zero
@@ -205,6 +207,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         pv(j);
         if (j + 2 < nt) qk(j + 2);
       }
+      tc::mma_commit(o_done);                          // the epilogue's one wait
 #ifdef CASCADE_PASS1_TRACE
       if (g_p1_trace) {
         const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -384,11 +387,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       if (EST && j > 0) est_readout(j - 1);
     }
     if (EST && nt > 0) est_readout(nt - 1);
-    // epilogue.  pv_done completes once per PV; when the last P is written only PV(nt-3) is
-    // known complete (QK(nt-1) followed it), so a parity wait for phase nt-1 alone could be
-    // satisfied by phase nt-3: wait for nt-2 first, then nt-1.
-    if (nt >= 2) tc::mbar_wait(pv_done, (nt - 2) & 1);
-    tc::mbar_wait(pv_done, (nt - 1) & 1);
+    // epilogue: o_done is committed once, after the last MMA (a parity wait on pv_done could
+    // not tell PV(nt-1) done from PV(nt-3) done: with EST the cs_done wait above lets PV(nt-1)
+    // finish first, and a wait for phase nt-2 then blocks forever)
+    tc::mbar_wait(o_done, 0);
 #ifdef CASCADE_PASS1_TRACE
     if (g_p1_trace && threadIdx.x == 128) {
       const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
