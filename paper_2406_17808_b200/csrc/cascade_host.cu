@@ -76,7 +76,7 @@ struct Sizes {
   size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk, s_heads;
   size_t maint_ctl;
   size_t per_layer;
-  size_t rope_tab, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
+  size_t rope_tab, rope_tab_f, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
   size_t total;
   int32_t plan_ints;
 };
@@ -108,13 +108,14 @@ Sizes compute_sizes(const cascade_config& c) {
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
                 z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl + z.s_heads;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
+  z.rope_tab_f = align_up((S + M) * (d / 2) * sizeof(float2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * d * sizeof(float2));   // [a][hi parts | lo parts]
   z.tab_lo = align_up(32 * d * sizeof(float2));
   z.stage_q = align_up(B * M * Hq * d * es);
   z.stage_kv = align_up(B * M * Hk * d * es);
   z.stage_out = z.stage_q;
   // two staging sets: the synchronous host call uses set 0, the pipelined one alternates
-  z.total = z.per_layer * c.num_layers + z.rope_tab + z.tab_hi + z.tab_lo +
+  z.total = z.per_layer * c.num_layers + z.rope_tab + z.rope_tab_f + z.tab_hi + z.tab_lo +
             2 * (z.stage_q + 2 * z.stage_kv + z.stage_out);
   return z;
 }
@@ -164,6 +165,7 @@ struct cascade_handle {
   std::vector<int32_t> m_last;
   std::vector<Pending> pending;   // per layer: an attend awaiting its commit
   double2* rope_tab;     // [S_tot + max_stride][d/2] (cos, sin)(pos theta_i) in fp64
+  float2* rope_tab_f;    // the same rounded to fp32 (rope_prep's fast path)
   float2* tab_hi;        // [npos/32 + 1][d] (cos, sin)(32 a theta_i) double-float: [d/2 hi | d/2 lo]
   float2* tab_lo;        // [32][d] (cos, sin)(b theta_i) double-float: [d/2 hi | d/2 lo]
   void *stage_q, *stage_k, *stage_v, *stage_out;           // set 0 (aliases stage[0])
@@ -354,6 +356,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.maint_barrier = 0;
   }
   h->rope_tab = reinterpret_cast<double2*>(take(sz.rope_tab));
+  h->rope_tab_f = reinterpret_cast<float2*>(take(sz.rope_tab_f));
   h->tab_hi = reinterpret_cast<float2*>(take(sz.tab_hi));
   h->tab_lo = reinterpret_cast<float2*>(take(sz.tab_lo));
   for (int i = 0; i < 2; ++i) {
@@ -418,6 +421,10 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
       }
     }
     ok = ok && cudaMemcpy(h->rope_tab, tab.data(), tab.size() * sizeof(double2),
+                          cudaMemcpyHostToDevice) == cudaSuccess;
+    std::vector<float2> tabf(tab.size());
+    for (size_t e = 0; e < tab.size(); ++e) tabf[e] = make_float2((float)tab[e].x, (float)tab[e].y);
+    ok = ok && cudaMemcpy(h->rope_tab_f, tabf.data(), tabf.size() * sizeof(float2),
                           cudaMemcpyHostToDevice) == cudaSuccess;
     // angle-addition factors for decode: pe = 32 a + b, cos/sin(32 a theta_i) and cos/sin(b theta_i)
     const size_t nhi = npos / 32 + 1;
@@ -678,7 +685,7 @@ cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, cons
   constexpr bool kTc = std::is_same<T, __nv_bfloat16>::value;
   {
     ProfScope ps(h, 0, st);
-    launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, q_rot, k_rot,
+    launch_rope_prep<T>(g, q, k, v, reinterpret_cast<const T*>(L.k_raw), h->rope_tab, h->rope_tab_f, q_rot, k_rot,
                         v_chunk, st);
     ps.finish(2.0 * es * g.d * ((double)g.B * g.Hq * m + (double)g.B * g.Hkv * (g.n_cached + 2.0 * m)));
   }

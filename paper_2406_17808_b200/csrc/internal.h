@@ -72,7 +72,7 @@ struct StateDev {
 // ---- launchers (defined in the .cu files) --------------------------------
 template <typename T>
 void launch_rope_prep(const Geometry& g, const T* q, const T* k, const T* v, const T* k_raw_state,
-                      const double2* rope_tab, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st);
+                      const double2* rope_tab, const float2* rope_tab_f, T* q_rot, T* k_rot, T* v_chunk, cudaStream_t st);
 
 template <typename T>
 void launch_attn_fwd_simt(const Geometry& g, const T* q_rot, const T* k_rot, const T* v_state,

@@ -31,13 +31,15 @@ def _bf(a):
     return torch.from_numpy(np.asarray(a)).to(torch.bfloat16)
 
 
-def _weights(seed, qk_scale=2.0):
+def _weights(seed, qk_scale=3.0):
     """Per layer (w_q, w_k, w_v, w_o) as bf16 values; q/k scaled up so attention is peaked
-    (selection margins, SURVEY 8(d) margin audit)."""
+    (selection margins, SURVEY 8(d) margin audit: seed 33 gives a minimum relative margin of
+    3.0e-3 over 1896 selections in the float64 stack), v and o scaled down so the residual stream
+    and the outputs stay at unit scale, where the north star's 2e-2 bf16 tolerance applies."""
     rng = np.random.default_rng(seed)
     s = 1.0 / np.sqrt(D_MODEL)
     shapes = [(D_MODEL, HQ * D_HEAD), (D_MODEL, HK * D_HEAD), (D_MODEL, HK * D_HEAD), (HQ * D_HEAD, D_MODEL)]
-    scales = [qk_scale * s, qk_scale * s, s, s]
+    scales = [qk_scale * s, qk_scale * s, 0.5 * s, 0.5 * s]
     ws = [[_bf(rng.standard_normal(sh) * sc) for sh, sc in zip(shapes, scales)] for _ in range(L)]
     return ws, rng
 
@@ -65,7 +67,7 @@ def _states_equal(a, b):
 
 def test_stack_wavefront_bit_identical_to_one_chunk_per_call():
     cfg = _cfg()
-    ws, rng = _weights(22)
+    ws, rng = _weights(33)
     T, m = 300, 32
     x = _bf(rng.standard_normal((B, T, D_MODEL))).cuda()
     cas_a, st_a = _stack(cfg, ws)
@@ -82,7 +84,7 @@ def test_stack_wavefront_bit_identical_to_one_chunk_per_call():
 
 def test_stack_every_layer_matches_oracle_given_its_inputs():
     cfg = _cfg()
-    ws, rng = _weights(22)
+    ws, rng = _weights(33)
     T, m = 300, 32
     x = _bf(rng.standard_normal((B, T, D_MODEL))).cuda()
     cas, st = _stack(cfg, ws)
