@@ -141,8 +141,7 @@ void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, c
                                         T*, float*, cudaStream_t);                              \
   template void launch_attn_score_simt<T>(const Geometry&, const T*, const T*, const float*,     \
                                           const float*, float*, cudaStream_t);
-INST(float)
-INST(__nv_bfloat16)
+INST(float)   // the fp32 path only: bf16 runs the tcgen05 kernels (k_attn_tc.cu)
 #undef INST
 
 }  // namespace cascade
