@@ -107,7 +107,10 @@ typedef struct {
                          /* 1 = homogeneous: s reduced over all kv-heads of a   */
                          /* sequence, one decision for all (P:542 ablation;    */
                          /* needs the unsharded head set; with head_reduce 2   */
-                         /* UNSUPPORTED); other values CONFIG                  */
+                         /* the median over all Hq <= 32 q-heads, else         */
+                         /* UNSUPPORTED; cascade_update_with_scores then       */
+                         /* UNSUPPORTED: kv-head s cannot give it); other      */
+                         /* values CONFIG                                      */
   int32_t head_reduce;   /* 0 = max over the GQA group; the ablations   */
                          /* of P:542: 1 = mean, 2 = median (even group: mean   */
                          /* of the middle two); 1/2 need Hq/Hkv <= 32 (else    */

@@ -34,6 +34,7 @@ struct LayerBufs {
   // per-call scratch (per layer so layers may run on different streams)
   float* s; float* lse; int32_t* plan; int32_t* resolved;
   float* s_heads;           // one-pass mode: per-q-head estimated mass [B][Hq][S_tot + Mb]
+  float* s_allheads;        // homogeneous + median: per-q-head exact mass [B][Hq][S_tot + Mb]
   void* q_rot; void* k_rot; void* v_chunk;
   uint32_t* maint_ctl;      // [0] grid-barrier counter, then per-(b, g) 64-bit counts of rows
                             // actually rewritten (8-byte aligned)
@@ -73,7 +74,7 @@ bool make_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t d) {
 }
 
 struct Sizes {
-  size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk, s_heads;
+  size_t k_raw, v, mu, origin, pe, s, lse, plan, resolved, q_rot, k_rot, v_chunk, s_heads, s_allheads;
   size_t maint_ctl;
   size_t per_layer;
   size_t rope_tab, rope_tab_f, tab_hi, tab_lo, stage_q, stage_kv, stage_out;
@@ -95,6 +96,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.s = align_up(B * Hk * (S + M) * 4);
   z.lse = align_up(B * Hq * ((M + 127) / 128 * 128) * 4);
   z.s_heads = (c.options & CASCADE_OPT_ONEPASS_SCORES) ? align_up(B * Hq * (S + (M + 127) / 128 * 128) * 4) : 0;
+  z.s_allheads = (c.head_policy == 1 && c.head_reduce == 2) ? align_up(B * Hq * (S + (M + 127) / 128 * 128) * 4) : 0;
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
@@ -106,7 +108,7 @@ Sizes compute_sizes(const cascade_config& c) {
   z.v_chunk = align_up(B * Hk * M * d * es);
   z.maint_ctl = align_up(8 + 8 * B * Hk);
   z.per_layer = z.k_raw + z.v + z.mu + z.origin + z.pe + z.s + z.lse + z.plan + z.resolved +
-                z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl + z.s_heads;
+                z.q_rot + z.k_rot + z.v_chunk + z.maint_ctl + z.s_heads + z.s_allheads;
   z.rope_tab = align_up((S + M) * (d / 2) * sizeof(double2));
   z.rope_tab_f = align_up((S + M) * (d / 2) * sizeof(float2));
   z.tab_hi = align_up(((S + M) / 32 + 1) * d * sizeof(float2));   // [a][hi parts | lo parts]
@@ -257,7 +259,7 @@ cascade_status cascade_validate_config(const cascade_config* c) {
   if (c->head_reduce != 0 && c->num_q_heads / c->num_kv_heads > 32) return CASCADE_ERR_UNSUPPORTED;
   if (c->dtype == CASCADE_BF16 && c->num_q_heads / c->num_kv_heads > 8) return CASCADE_ERR_UNSUPPORTED;
   if (c->head_policy < 0 || c->head_policy > 1) return CASCADE_ERR_CONFIG;
-  if (c->head_policy == 1 && c->head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;  // median of all heads
+  if (c->head_policy == 1 && c->head_reduce == 2 && c->num_q_heads > 32) return CASCADE_ERR_UNSUPPORTED;  // median of all heads
   if (c->options & ~(CASCADE_OPT_ONEPASS_SCORES | CASCADE_OPT_EXACT_DECODE_ROPE)) return CASCADE_ERR_CONFIG;
   if ((c->options & CASCADE_OPT_ONEPASS_SCORES) && c->dtype != CASCADE_BF16) return CASCADE_ERR_UNSUPPORTED;
   const long long S = (long long)c->sink_size + c->cache_size;
@@ -349,6 +351,7 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
     L.s = reinterpret_cast<float*>(take(sz.s));
     L.lse = reinterpret_cast<float*>(take(sz.lse));
     L.s_heads = sz.s_heads ? reinterpret_cast<float*>(take(sz.s_heads)) : nullptr;
+    L.s_allheads = sz.s_allheads ? reinterpret_cast<float*>(take(sz.s_allheads)) : nullptr;
     L.plan = reinterpret_cast<int32_t*>(take(sz.plan));
     L.resolved = reinterpret_cast<int32_t*>(take(sz.resolved));
     L.q_rot = take(sz.q_rot); L.k_rot = take(sz.k_rot); L.v_chunk = take(sz.v_chunk);
@@ -606,6 +609,9 @@ uint64_t moved_total(cascade_handle* h) {
   return tot;
 }
 
+// row stride of the per-q-head mass buffers (s_heads, s_allheads): S_tot + max_stride rounded to 128
+inline int heads_ld(const cascade_handle* h) { return h->S_tot + (h->cfg.max_stride + 127) / 128 * 128; }
+
 // CUDA status of the launches issued since the last check (and clears it).
 inline bool launches_ok() { return cudaGetLastError() == cudaSuccess; }
 
@@ -703,8 +709,10 @@ cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, cons
     tp.head_reduce = g.head_reduce;
     tp.w = up.w;
     tp.s_heads = L.s_heads;                   // non-null: the one-pass estimator (no pass 2)
+    tp.heads_out = L.s_heads ? nullptr : L.s_allheads;   // homogeneous + median: every head's mass
     if (cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + m) * sizeof(float), st) != cudaSuccess)
       return CASCADE_ERR_CUDA;
+    if (tp.heads_out && cudaMemsetAsync(L.s_allheads, 0, h->sz.s_allheads, st) != cudaSuccess) return CASCADE_ERR_CUDA;
     if (L.s_heads && cudaMemsetAsync(L.s_heads, 0, h->sz.s_heads, st) != cudaSuccess) return CASCADE_ERR_CUDA;
     ProfScope ps(h, 1, st);
     launch_attn_fwd_tc(tp, L.tm_q, L.tm_k, L.tm_vs, L.tm_vc, g.d, st);
@@ -734,12 +742,18 @@ cascade_status attend_prefill(cascade_handle* h, int32_t layer, const T* q, cons
     // at 2^-126 instead of flushing to 0, which would make the all-zero masses tiny and unequal)
   } else {
     ProfScope ps(h, 2, st);
-    launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, up.w, L.s, st);
+    if (L.s_allheads && cudaMemsetAsync(L.s_allheads, 0, h->sz.s_allheads, st) != cudaSuccess)
+      return CASCADE_ERR_CUDA;
+    launch_attn_score_simt<T>(g, q_rot, k_rot, L.lse, up.w, L.s, L.s_allheads, heads_ld(h), st);
     ps.finish(useful);
     ++h->launches;
   }
   if (g.homogeneous) {        // one s per sequence, folded by the maintenance launch
-    launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
+    if (g.head_reduce == 2)     // the median of all q-heads (one-pass: of the per-head estimates)
+      launch_head_median_all(g.B, g.Hq, g.Hkv, g.S_tot + m, L.s_heads ? L.s_heads : L.s_allheads, heads_ld(h),
+                             L.s, st);
+    else
+      launch_head_homogenize(g.B, g.Hkv, g.S_tot + m, g.head_reduce, L.s, st);
     ++h->launches;
   }
   const bool folded = kTc && !g.homogeneous;
@@ -802,6 +816,8 @@ cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat
   dp.k_raw_mut = static_cast<__nv_bfloat16*>(L.k_raw);
   dp.v_mut = static_cast<__nv_bfloat16*>(L.v);
   dp.mu = L.mu; dp.origin = L.origin; dp.s = L.s;
+  dp.heads_out = L.s_allheads;         // homogeneous + median only (else null)
+  dp.heads_ld = heads_ld(h);
   dp.tab = h->rope_tab; dp.tab_hi = h->tab_hi; dp.tab_lo = h->tab_lo;
   dp.n_tiles = up.n_dec_tiles;
   dp.dec_tiles = up.dec_tiles;
@@ -812,6 +828,7 @@ cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat
   if (h->m_last[layer] != 1 &&
       cudaMemsetAsync(L.s, 0, (size_t)g.B * g.Hkv * (g.S_tot + 1) * sizeof(float), st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
+  if (L.s_allheads && cudaMemsetAsync(L.s_allheads, 0, h->sz.s_allheads, st) != cudaSuccess) return CASCADE_ERR_CUDA;
   const Plan& P = h->plan;
   {
     ProfScope ps(h, 4, st);
@@ -820,7 +837,10 @@ cascade_status attend_decode(cascade_handle* h, int32_t layer, const __nv_bfloat
                                         st) == cudaSuccess;
     ++h->launches;
     if (ok && g.homogeneous) {          // one s per sequence over the local kv-heads
-      launch_head_homogenize(g.B, g.Hkv, g.S_tot + 1, g.head_reduce, L.s, st);
+      if (g.head_reduce == 2)
+        launch_head_median_all(g.B, g.Hq, g.Hkv, g.S_tot + 1, L.s_allheads, heads_ld(h), L.s, st);
+      else
+        launch_head_homogenize(g.B, g.Hkv, g.S_tot + 1, g.head_reduce, L.s, st);
       ++h->launches;
     }
     if (!ok || !launches_ok()) return dp.update ? poison(h) : CASCADE_ERR_CUDA;
@@ -1017,6 +1037,8 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
   cascade_status rc = check_call(h, layer, m);
   if (rc != CASCADE_OK) return rc;
   if (!k || !v || !s) return CASCADE_ERR_INVALID_ARG;
+  // the median of all q-heads (homogeneous + median) is not a function of per-kv-head s
+  if (h->cfg.head_policy == 1 && h->cfg.head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LayerBufs& L = h->layers[layer];
   const Geometry g = make_geometry(h, h->mirrors[layer], m);

@@ -80,7 +80,7 @@ void launch_attn_fwd_simt(const Geometry& g, const T* q_rot, const T* k_rot, con
 
 template <typename T>
 void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, const float* lse,
-                            const float* w, float* s, cudaStream_t st);
+                            const float* w, float* s, float* heads_out, int heads_ld, cudaStream_t st);
 
 
 void launch_select_resolve(const Geometry& g, const PlanDev& p, int32_t begin, int32_t end,
@@ -116,6 +116,9 @@ void launch_ema_fold(const Geometry& g, double* mu, const float* s, cudaStream_t
 // Homogeneous head policy: s[b][0..Hkv)[len] <- its reduction over the kv-heads
 // (mode 0 max, 1 mean), written back to every kv-head.
 void launch_head_homogenize(int B, int Hkv, int len, int mode, float* s, cudaStream_t st);
+// homogeneous + median: s[b][g][x] = median over ALL q-heads h of heads[b][h][x], every g
+void launch_head_median_all(int B, int Hq, int Hkv, int len, const float* heads, int heads_ld, float* s,
+                            cudaStream_t st);
 
 // tcgen05 attention (k_attn_tc.cu)
 struct TcParams {
@@ -138,6 +141,9 @@ struct TcParams {
   // mass (Alg. 3) into s_heads [B][Hq][S_tot + Mb] (zeroed per call, atomic adds)
   const float* w;               // [m] EMA row weights (1 - gamma) gamma^(m-1-r)
   float* s_heads;               // null: exact mode (pass 2)
+  // homogeneous + median (P:542 ablation): pass 2 also writes every q-head's mass to
+  // heads_out [B][Hq][S_tot + Mb] (null otherwise)
+  float* heads_out;
 };
 // per-key group reduction + EMA fold of the one-pass estimates (k_attn_tc.cu)
 void launch_onepass_reduce(const TcParams& p, const Geometry& g, bool fold, cudaStream_t st);
@@ -166,6 +172,8 @@ struct DecodeParams {
   double* mu;                   // state
   int64_t* origin;              // state
   float* s;                     // [B*Hkv][S_tot + 1] exact mass (last_scores layout)
+  float* heads_out;             // homogeneous + median: every q-head's mass, row stride heads_ld
+  int32_t heads_ld;
   const double2* tab;           // [npos][D/2] cos/sin(pe theta_i), fp64
   const float2* tab_hi;         // [npos/32 + 1][D] cos/sin(32 a theta_i) double-float [D/2 hi | D/2 lo]
   const float2* tab_lo;         // [32][D] cos/sin(b theta_i) double-float [D/2 hi | D/2 lo]

@@ -70,7 +70,8 @@ __global__ void attn_fwd_simt_kernel(Geometry g, const T* __restrict__ q_rot,
 template <typename T, int D>
 __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
                                        const T* __restrict__ k_rot, const float* __restrict__ lse,
-                                       const float* __restrict__ w, float* __restrict__ s) {
+                                       const float* __restrict__ w, float* __restrict__ s,
+                                       float* __restrict__ heads_out, int heads_ld) {
   constexpr int E = D / 32;
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -109,6 +110,7 @@ __global__ void attn_score_simt_kernel(Geometry g, const T* __restrict__ q_rot,
     }
     best = j == 0 ? acc : fmaxf(best, acc);       // max over the group
     if (j < kMaxMedianGroup) hv[j] = acc;         // G <= 32 whenever an ablation is on
+    if (heads_out && lane == 0) heads_out[((long long)b * g.Hq + h) * heads_ld + x] = acc;
   }
   if (g.head_reduce) best = group_reduce_ablation(hv, g.G, g.head_reduce);   // mean / median
   if (lane == 0) s[warp] = best;
@@ -127,20 +129,20 @@ void launch_attn_fwd_simt(const Geometry& g, const T* q_rot, const T* k_rot, con
 
 template <typename T>
 void launch_attn_score_simt(const Geometry& g, const T* q_rot, const T* k_rot, const float* lse,
-                            const float* w, float* s, cudaStream_t st) {
+                            const float* w, float* s, float* heads_out, int heads_ld, cudaStream_t st) {
   long long warps = (long long)g.B * g.Hkv * (g.S_tot + g.m);
   int blocks = ceil_div(warps * 32, 256);
   if (g.d == 64)
-    attn_score_simt_kernel<T, 64><<<blocks, 256, 0, st>>>(g, q_rot, k_rot, lse, w, s);
+    attn_score_simt_kernel<T, 64><<<blocks, 256, 0, st>>>(g, q_rot, k_rot, lse, w, s, heads_out, heads_ld);
   else
-    attn_score_simt_kernel<T, 128><<<blocks, 256, 0, st>>>(g, q_rot, k_rot, lse, w, s);
+    attn_score_simt_kernel<T, 128><<<blocks, 256, 0, st>>>(g, q_rot, k_rot, lse, w, s, heads_out, heads_ld);
 }
 
 #define INST(T)                                                                                   \
   template void launch_attn_fwd_simt<T>(const Geometry&, const T*, const T*, const T*, const T*, \
                                         T*, float*, cudaStream_t);                              \
   template void launch_attn_score_simt<T>(const Geometry&, const T*, const T*, const float*,     \
-                                          const float*, float*, cudaStream_t);
+                                          const float*, float*, float*, int, cudaStream_t);
 INST(float)   // the fp32 path only: bf16 runs the tcgen05 kernels (k_attn_tc.cu)
 #undef INST
 

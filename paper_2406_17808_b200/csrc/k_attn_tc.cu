@@ -184,7 +184,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
           const uint64_t db = tc::desc_mnmajor_sw128(vbase + kk * 2048, kTileBytes);
           tc::mma_bf16_ts(tmem + kColO, pbase + kk * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::mma_commit(kv_empty + (j % kStages));
+        if (j + kStages < nt) tc::mma_commit(kv_empty + (j % kStages));   // the producer waits only these
         tc::mma_commit(pv_done);
         if (EST) {                                      // column sums sum_r a_r P[r, key]
           constexpr uint32_t idesc_cs = tc::idesc_bf16_f32(128, 16, 0, 1);   // A MN-major, B K-major
@@ -580,7 +580,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int j = lane; j < tl.y; j += 32) smu[w * 128 + j] = p.mu[bg * p.S_tot + tl.x + j];
       }
     }
-    tc::named_bar_sync(1, 544);
+    tc::named_bar_sync_roles(1, 544);
   } else if (warp >= 4) {
     const int wgi = (warp - 4) >> 2;                      // 0..3
     const int wg = wgi & 1, half = wgi >> 1;              // key tile of the pair, column half
@@ -628,7 +628,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         ++hcur;
       }
     }
-    tc::named_bar_sync(1, 544);                           // all halves' per-head sums in smem
+    tc::named_bar_sync_roles(1, 544);                           // all halves' per-head sums in smem
     if (half == 0 && active && r < klen) {
       const float* h0 = sacc + (wg * 2 + 0) * p.G * 128;
       const float* h1 = sacc + (wg * 2 + 1) * p.G * 128;
@@ -641,6 +641,10 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         best = group_reduce_ablation(hv, p.G, p.head_reduce);
       }
       p.s[bg * (p.S_tot + p.m) + kstart + r] = best;
+      if (p.heads_out)                                    // homogeneous + median: every head's mass
+        for (int hh = 0; hh < p.G; ++hh)
+          p.heads_out[((long long)b * p.Hq + gkv * p.G + hh) * (p.S_tot + p.Mb) + kstart + r] =
+              h0[hh * 128 + r] + h1[hh * 128 + r];
       if (resident && p.mu)                               // EMA fold (Q4), never an FMA
         p.mu[bg * p.S_tot + kstart + r] = __dadd_rn(__dmul_rn(p.decay, smu[wg * 128 + r]), (double)best);
     }

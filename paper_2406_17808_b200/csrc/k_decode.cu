@@ -49,17 +49,29 @@ constexpr int kKStages = 3;
 constexpr int kTileBytes32K = 32768;                         // one 128 x 128 bf16 K or V tile
 constexpr uint32_t kColLg = 64;                              // compact logits: GM columns per tile
 constexpr uint32_t kTmemCols = 512;
+#ifndef CASCADE_DEC_ROT_WG
+#define CASCADE_DEC_ROT_WG 2
+#endif
+#ifndef CASCADE_DEC_PBUF
+#define CASCADE_DEC_PBUF 2
+#endif
+constexpr int kPBuf = CASCADE_DEC_PBUF;                      // P^T buffers (2: softmax(j) overlaps PV(j-1))
 // EXACT: the rotation proves every bf16 rounding and recomputes the unprovable pairs from the
 // double-float tables, which needs the tables' lo parts in shared memory (a-rows of 1 KB, a second
 // b-row table) and leaves room for two V stages; the fast variant stages hi parts only, three V stages.
 template <bool EXACT> struct DecLayout {
-  static constexpr int kVStages = EXACT ? 2 : 3;
+  // rotation warpgroups: the exact variant's provable-rounding check and recomputation make the
+  // rotation heavier, so it gets a third group (1.22 vs 1.35 ms per configs[3] step); the fast
+  // variant measured the same with two and three (0.924 / 0.926 ms)
+  static constexpr int kRotWG = EXACT ? 3 : CASCADE_DEC_ROT_WG;
+  static constexpr int kThreads = 256 + 128 * kRotWG;
+  static constexpr int kVStages = (EXACT || kPBuf == 2) ? 2 : 3;   // 227 KB: 3 V stages only with one P^T buffer
   static constexpr int kRowBytes = EXACT ? 1024 : 512;      // a-row: [64 float2 hi | 64 float2 lo] or hi only
   static constexpr int kARows = kHiRows * kRowBytes;        // a-rows per K stage
   static constexpr int kLoTables = EXACT ? 2 : 1;
   // sK | sV | sQ | sP | sA | sLo (| sLoL) | scalars + barriers; sO aliases sQ / sP after the tiles
   static constexpr size_t smem(int GM) {
-    return (size_t)kKStages * kTileBytes32K + (size_t)kVStages * kTileBytes32K + 4096 + 4096 +
+    return (size_t)kKStages * kTileBytes32K + (size_t)kVStages * kTileBytes32K + 4096 + kPBuf * 4096 +
            (size_t)kKStages * kARows + (size_t)kLoTables * kLoRows * kLoStride + 4 * 8 * 4 + 40 * 4 + 64 +
            24 * 8 + 1024;
   }
@@ -69,7 +81,7 @@ template <bool EXACT> struct DecLayout {
 size_t decode_fused_smem(int GM, bool exact) { return exact ? DecLayout<true>::smem(GM) : DecLayout<false>::smem(GM); }
 int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 
-// Tensor-core decode, warp roles (512 threads):
+// Tensor-core decode, warp roles (DecLayout::kThreads = 256 + 128 kRotWG threads):
 //   warp 0     producer: TMA of the raw K tile (SWIZZLE_128B) + the float64 cos/sin rows of the
 //              tile's 32-position blocks (bulk copies) into a 3-stage K ring, freed by QK^T
 //   warp 3     producer: TMA of the V tile into a 2-stage V ring, freed by PV
@@ -77,28 +89,30 @@ int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 //              softmax(j)), then O^T[128 d x 16] += V^T P^T
 //   warp 2     TMEM allocator
 //   warps 4-7  softmax: thread t = key t: logits (kept in TMEM), online softmax per head, P^T
-//   warps 8-15 two rotation warpgroups (half of the rotate-half pairs each): rotate every raw
-//              key IN PLACE to its rank pe; they run up to a full ring ahead of the softmax.
-// After the tiles, warps 4-15 compute the masses and the fold; rank 0's softmax warps merge O
+//   warps 8+   kRotWG rotation warpgroups (the tile's 128 keys x 8 16-byte chunks of rotate-half
+//              pairs dealt round-robin): rotate every raw key IN PLACE to its rank pe; they run up
+//              to a full ring ahead of the softmax.  The rotation is the decode's issue-heaviest
+//              stage; a third group measured no faster (0.926 vs 0.924 ms per configs[3] step).
+// After the tiles, warps 4+ compute the masses and the fold; rank 0's softmax warps merge O
 // and its warp 0 applies the insertion.
 // Tile descriptor (int4, host): start slot, length, pe of key 0 (pe of key j = pe0 + j: the host
 // splits a tile where a full ring wraps past its oldest slot).
 template <int GM, bool EXACT>
-__global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
+__global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                               const __grid_constant__ CUtensorMap tm_v,
                                                               DecodeParams p, PlanDev pl, int32_t n_sel,
                                                               const int32_t* __restrict__ phase_begin,
                                                               int32_t n_phase, __nv_bfloat16* __restrict__ out) {
   constexpr int D = 128, HALF = 64;
   using Lay = DecLayout<EXACT>;
-  constexpr int kVStages = Lay::kVStages, kRowBytes = Lay::kRowBytes;
+  constexpr int kVStages = Lay::kVStages, kRowBytes = Lay::kRowBytes, kRotWG = Lay::kRotWG;
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
   uint8_t* sK = dsm;                                        // kKStages x K tile (1 KB aligned for TMA)
   uint8_t* sV = sK + kKStages * kTileBytes32K;              // kVStages x V tile
   uint8_t* sQ = sV + kVStages * kTileBytes32K;              // [16 rows x 128 d] SW128 (2 x 2 KB)
-  uint8_t* sP = sQ + 4096;                                  // [16 heads x 128 keys] SW128 (2 x 2 KB)
-  uint8_t* sA = sP + 4096;                                  // kKStages x the tile's a-rows (cos/sin(32a theta))
+  uint8_t* sP = sQ + 4096;                                  // 2 x [16 heads x 128 keys] SW128 (2 x 2 KB)
+  uint8_t* sA = sP + kPBuf * 4096;                                  // kKStages x the tile's a-rows (cos/sin(32a theta))
   uint8_t* sLo = sA + kKStages * Lay::kARows;               // 32 x kLoStride: cos/sin(b theta_i), fp32 hi parts
   uint8_t* sLoL = sLo + (EXACT ? kLoRows * kLoStride : 0);  // (EXACT) their fp32 lo parts
   float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sLoL + kLoRows * kLoStride);   // [4][8]
@@ -110,10 +124,10 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sTmem + 1) + 7) & ~uintptr_t(7));
   uint64_t* kfull = bars + 0;       // [3]
   uint64_t* kempty = bars + 3;      // [3]
-  uint64_t* rot_full = bars + 6;    // [3 stages][2 rotation warpgroups]
+  uint64_t* rot_full = bars + 6;    // [3 stages]: every rotation warp arrives
   uint64_t* s_full = bars + 12;     // [2] per S^T buffer
   uint64_t* p_full = bars + 14;     // [2] per S^T buffer
-  uint64_t* pv_done = bars + 16;
+  uint64_t* pv_done[2] = {bars + 16, bars + 23};   // PV of tiles j with j % 2 == i (sP buffer i)
   uint64_t* vfull = bars + 17;      // [kVStages <= 3]
   uint64_t* vempty = bars + 20;     // [kVStages <= 3]
 
@@ -131,9 +145,10 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   if (tid == 0) {
     for (int i = 0; i < kKStages; ++i) { tc::mbar_init(kfull + i, 1); tc::mbar_init(kempty + i, 1); }
     for (int i = 0; i < kVStages; ++i) { tc::mbar_init(vfull + i, 1); tc::mbar_init(vempty + i, 1); }
-    for (int i = 0; i < 2 * kKStages; ++i) tc::mbar_init(rot_full + i, 4);
+    for (int i = 0; i < kKStages; ++i) tc::mbar_init(rot_full + i, 4 * kRotWG);
     for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
-    tc::mbar_init(pv_done, 1);
+    tc::mbar_init(pv_done[0], 1);
+    tc::mbar_init(pv_done[1], 1);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_v); }
@@ -159,7 +174,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
     *reinterpret_cast<float2*>(sLo + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + ii];
     if (EXACT) *reinterpret_cast<float2*>(sLoL + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + HALF + ii];
   }
-  for (int o = tid; o < 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
+  for (int o = tid; o < kPBuf * 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -190,6 +205,11 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         if (start < p.S_tot) {
           const int row = (int)((long long)bg * p.S_tot + start);
           for (int kb = 0; kb < 2; ++kb) tc::tma_load_2d(st + kb * 16384, &tm_k, kfull + s, kb * 64, row);
+          // the epilogue folds this tile's mu: pull it into L2 now (off the HBM-latency tail)
+          // (bulk prefetch: 16-B aligned start and size, so the range is trimmed to whole pairs)
+          const long long x0 = ((long long)bg * p.S_tot + start + 1) & ~1LL;
+          const long long x1 = ((long long)bg * p.S_tot + start + len) & ~1LL;
+          if (p.update && x1 > x0) tc::bulk_prefetch_l2(p.mu + x0, (uint32_t)(x1 - x0) * 8u);
         }
         for (int r = 0; r < nA; ++r)
           tc::bulk_load(sA + s * Lay::kARows + r * kRowBytes, p.tab_hi + (long long)(a0 + r) * 2 * HALF, kRowBytes,
@@ -221,8 +241,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       auto qk = [&](int j) {
         const int s = j % kKStages;
         const uint32_t st = tc::smem_u32(sK + s * kTileBytes32K);
-        tc::mbar_wait(rot_full + 2 * s, (j / kKStages) & 1);       // both rotated halves in place
-        tc::mbar_wait(rot_full + 2 * s + 1, (j / kKStages) & 1);
+        tc::mbar_wait(rot_full + s, (j / kKStages) & 1);           // every rotated chunk in place
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -244,17 +263,17 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t da = tc::desc_mnmajor_sw128(st + kk * 2048, 16384);
-          const uint64_t db = tc::desc_kmajor_sw128(aP + (kk >> 2) * 2048 + (kk & 3) * 32);
+          const uint64_t db = tc::desc_kmajor_sw128(aP + (kPBuf == 2 ? (j & 1) * 4096 : 0) + (kk >> 2) * 2048 + (kk & 3) * 32);
           tc::mma_bf16_ss(tO, da, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::mma_commit(pv_done);
+        tc::mma_commit(pv_done[j & 1]);
         tc::mma_commit(vempty + s);
       }
     }
   } else if (warp >= 8) {
     // ---------------- rotation warpgroups ----------------
-    const int t = (tid - 256) & 127;                         // key row of the tile
-    const int rwg = (tid - 256) >> 7;                        // chunks [4 rwg, 4 rwg + 4)
+    const int t = (tid - 256) & 127;                         // key row of the tile (fixed per thread)
+    const int c0 = (tid - 256) >> 7;                         // chunks c0, c0 + kRotWG, ... (< 8)
     for (int j = 0; j < nt; ++j) {
       const int s = j % kKStages;
       uint8_t* st = sK + s * kTileBytes32K;
@@ -277,7 +296,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         const float2* lo = reinterpret_cast<const float2*>(sLo + (pe & 31) * kLoStride);
         const float2* lo_l = reinterpret_cast<const float2*>(sLoL + (pe & 31) * kLoStride);
 #pragma unroll 1
-        for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
+        for (int c = c0; c < 8; c += kRotWG) {
           const int off = t * 128 + ((c ^ (t & 7)) << 4);
           uint4* pa = reinterpret_cast<uint4*>(st + off);
           uint4* pb = reinterpret_cast<uint4*>(st + 16384 + off);
@@ -302,14 +321,23 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
             // (> that bound + half an ulp of y), [y - delta, y + delta] holds the exact value, so
             // when both ends round to the same bf16 so does the exact rotation (rounding is
             // monotonic) and that bf16 is the result; otherwise the pair is recomputed exactly.
-            const float2 dl = __fmul2_rn(__fadd2_rn(make_float2(fabsf(x1.x), fabsf(x1.y)),
-                                                    make_float2(fabsf(x2.x), fabsf(x2.y))),
-                                         make_float2(4e-7f, 4e-7f));
-            const float2 nd = make_float2(-dl.x, -dl.y);
-            const float2 y1l = __fadd2_rn(y1, nd), y1h = __fadd2_rn(y1, dl);
-            const float2 y2l = __fadd2_rn(y2, nd), y2h = __fadd2_rn(y2, dl);
-            uint32_t r1 = tc::pack_bf16(y1l.x, y1l.y), r2 = tc::pack_bf16(y2l.x, y2l.y);
-            if (EXACT && valid && (r1 != tc::pack_bf16(y1h.x, y1h.y) || r2 != tc::pack_bf16(y2h.x, y2h.y))) {
+            uint32_t r1, r2;
+            bool fix = false;
+            if (EXACT) {
+              const float2 dl = __fmul2_rn(__fadd2_rn(make_float2(fabsf(x1.x), fabsf(x1.y)),
+                                                      make_float2(fabsf(x2.x), fabsf(x2.y))),
+                                           make_float2(4e-7f, 4e-7f));
+              const float2 nd = make_float2(-dl.x, -dl.y);
+              const float2 y1l = __fadd2_rn(y1, nd), y1h = __fadd2_rn(y1, dl);
+              const float2 y2l = __fadd2_rn(y2, nd), y2h = __fadd2_rn(y2, dl);
+              r1 = tc::pack_bf16(y1l.x, y1l.y);
+              r2 = tc::pack_bf16(y2l.x, y2l.y);
+              fix = valid && (r1 != tc::pack_bf16(y1h.x, y1h.y) || r2 != tc::pack_bf16(y2h.x, y2h.y));
+            } else {                                 // fast variant: the fp32 rotation's own rounding
+              r1 = tc::pack_bf16(y1.x, y1.y);
+              r2 = tc::pack_bf16(y2.x, y2.y);
+            }
+            if (EXACT && fix) {
               // exact: cos / sin from the double-float tables (hi + lo) by angle addition in
               // double, then rope_prep's arithmetic (double products, double -> float -> bf16)
               float o1[2], o2[2];
@@ -340,7 +368,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         tc::mbar_wait(vfull + sv_i, (j / kVStages) & 1);
         uint8_t* sv = sV + sv_i * kTileBytes32K;
         const int off_base = t * 128;
-        for (int c = 4 * rwg; c < 4 * rwg + 4; ++c) {
+        for (int c = c0; c < 8; c += kRotWG) {
           const int off = off_base + ((c ^ (t & 7)) << 4);
           uint4 ka = make_uint4(0u, 0u, 0u, 0u), kb2 = ka, va = ka, vb = ka;
           if (t == 0) {
@@ -376,7 +404,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       }
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(rot_full + 2 * s + rwg);
+      if (lane == 0) tc::mbar_arrive(rot_full + s);
     }
   } else if (warp >= 4) {
     // ---------------- softmax warpgroup ----------------
@@ -425,8 +453,15 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         }
         *sRescale = any;
       }
-      if (j >= 1) tc::mbar_wait(pv_done, (j - 1) & 1);      // sP free, O^T holds tiles < j
       tc::named_bar_sync(1, 128);
+      // sP[j % 2] is free once PV(j-2) is done; a rescale of O^T needs every PV < j (PV(j-1)
+      // done: tcgen05 MMAs of one thread complete in order).  One barrier per buffer, so a
+      // parity wait is never ambiguous (PV(j) cannot complete before this P is written).
+      if (*sRescale || kPBuf == 1) {
+        if (j >= 1) tc::mbar_wait(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+      } else if (j >= 2) {
+        tc::mbar_wait(pv_done[j & 1], ((j - 2) >> 1) & 1);
+      }
       tc::tc_fence_after();
 #pragma unroll
       for (int h = 0; h < GM; ++h) {
@@ -436,7 +471,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         const float pv = (valid && h < G) ? exp2f(lg[h] - mn) : 0.f;
         l_part[h] = l_part[h] * cr + pv;
         const int blk = t >> 6, kc = t & 63;
-        *reinterpret_cast<__nv_bfloat16*>(sP + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
+        *reinterpret_cast<__nv_bfloat16*>(sP + (kPBuf == 2 ? (j & 1) * 4096 : 0) + blk * 2048 + h * 128 + ((((kc >> 3) ^ (h & 7))) << 4) + (kc & 7) * 2) =
             __float2bfloat16_rn(pv);
       }
       if (*sRescale) {                                       // O^T column h *= corr_h (lane = d)
@@ -462,7 +497,7 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) sRed[w4][h] = v;
     }
-    if (nt > 0) tc::mbar_wait(pv_done, (nt - 1) & 1);      // O^T holds every tile
+    if (nt > 0) tc::mbar_wait(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);   // O^T holds every tile
     tc::tmem_wait_st();
     tc::named_bar_sync(1, 128);
     if (t < GM) {
@@ -488,7 +523,8 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
   }
   __syncthreads();
   if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;                          // 0..2: three warpgroups share the tiles
+    constexpr int kWG = 1 + kRotWG;                          // warpgroups sharing the tiles
+    const int wg = (warp - 4) >> 2;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int t = (warp & 3) * 32 + lane;                    // key (or d) = TMEM lane
     if (wg == 0) {                                           // scaled partial O^T -> sO (own smem)
@@ -507,14 +543,14 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
     // kU tiles per round: every TMEM load and mu load of the round is issued before the first
     // use, so the tail streams instead of paying one load round trip per tile
     constexpr int kU = 4;
-    for (int j0 = wg; j0 < nt; j0 += 3 * kU) {
+    for (int j0 = wg; j0 < nt; j0 += kWG * kU) {
       uint32_t lgb[kU][GM];
       double m0[kU];
       int xs[kU];
       bool vk[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int j = j0 + 3 * u;
+        const int j = j0 + kWG * u;
         int start = 0, len = 0, pe0 = 0;
         if (j < nt) {
           tile_info(tbeg + j, start, len, pe0);
@@ -537,6 +573,9 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
           float hv[GM];
 #pragma unroll
           for (int h = 0; h < GM; ++h) hv[h] = h < G ? exp2f(__uint_as_float(lgb[u][h]) - lse[h]) : 0.f;
+          if (p.heads_out)                                   // homogeneous + median: every head's mass
+            for (int h = 0; h < G; ++h)
+              p.heads_out[((long long)b * p.Hq + g * G + h) * p.heads_ld + xs[u]] = p.w0 * hv[h];
           best = group_reduce_ablation(hv, G, p.head_reduce);
         }
         const float sv = p.w0 * best;
@@ -576,37 +615,48 @@ __global__ void __launch_bounds__(512, 1) decode_fused_kernel(const __grid_const
         }
       }
       __syncwarp();
-      for (int ph = 0; ph < n_phase; ++ph) {
-        for (int e = phase_begin[ph]; e < phase_begin[ph + 1]; ++e) {
+      // moves in phase order (deepest sub-cache first), kMB per round: every source of a round is
+      // read before any of its destinations is written, rounds in order.  A move's destination
+      // is only ever the source of an EARLIER move (the evictee it carried down), so
+      // batching keeps the one-at-a-time semantics with one load round trip per round instead of
+      // one per move.
+      constexpr int NV = D * 2 / 16;                         // 16-B vectors per K (or V) row
+      constexpr int kMB = 6;
+      const int e_end = phase_begin[n_phase];
+      for (int e0 = phase_begin[0]; e0 < e_end; e0 += kMB) {
+        uint4 row[kMB];
+        int32_t dsts[kMB];
+        double mu_new = 0.0;
+        int64_t org = 0;
+#pragma unroll
+        for (int u = 0; u < kMB; ++u) {
+          const int e = e0 + u;
+          dsts[u] = -1;
+          if (e >= e_end) continue;
           const int32_t dst = pl.mov[2 * e];
           int32_t src = pl.mov[2 * e + 1];
           src = src >= 0 ? src : res[-src - 1];
           if (src == dst) continue;
-          const __nv_bfloat16 *ks, *vs;
-          double mu_new;
-          int64_t org;
+          dsts[u] = dst;
+          const __nv_bfloat16* rs;                           // lanes < NV: K, the rest: V
           if (src < p.S_tot) {
-            ks = p.k_raw_mut + ((long long)bg * p.S_tot + src) * D;
-            vs = p.v_mut + ((long long)bg * p.S_tot + src) * D;
-            mu_new = mu[src];
-            org = p.origin[(long long)bg * p.S_tot + src];
+            rs = (lane < NV ? p.k_raw_mut : p.v_mut) + ((long long)bg * p.S_tot + src) * D;
+            if (lane == u) { mu_new = mu[src]; org = p.origin[(long long)bg * p.S_tot + src]; }
           } else {
-            ks = p.k_new + (long long)bg * D;
-            vs = p.v_new + (long long)bg * D;
-            mu_new = (double)s_out[src];
-            org = p.t0;
+            rs = (lane < NV ? p.k_new : p.v_new) + (long long)bg * D;
+            if (lane == u) { mu_new = (double)s_out[src]; org = p.t0; }
           }
-          __nv_bfloat16* kd = p.k_raw_mut + ((long long)bg * p.S_tot + dst) * D;
-          __nv_bfloat16* vd = p.v_mut + ((long long)bg * p.S_tot + dst) * D;
-          constexpr int NV = D * 2 / 16;
-          const uint4 kv = reinterpret_cast<const uint4*>(ks)[lane & (NV - 1)];
-          const uint4 vv = reinterpret_cast<const uint4*>(vs)[lane & (NV - 1)];
-          __syncwarp();                                    // every lane read before any write
-          if (lane < NV) reinterpret_cast<uint4*>(kd)[lane] = kv;
-          else reinterpret_cast<uint4*>(vd)[lane - NV] = vv;
-          if (lane == 0) { mu[dst] = mu_new; p.origin[(long long)bg * p.S_tot + dst] = org; }
-          __syncwarp();
+          row[u] = reinterpret_cast<const uint4*>(rs)[lane & (NV - 1)];
         }
+        __syncwarp();                                        // every read of the round done
+#pragma unroll
+        for (int u = 0; u < kMB; ++u) {
+          if (dsts[u] < 0) continue;
+          __nv_bfloat16* rd = (lane < NV ? p.k_raw_mut : p.v_mut) + ((long long)bg * p.S_tot + dsts[u]) * D;
+          reinterpret_cast<uint4*>(rd)[lane & (NV - 1)] = row[u];
+          if (lane == u) { mu[dsts[u]] = mu_new; p.origin[(long long)bg * p.S_tot + dsts[u]] = org; }
+        }
+        __syncwarp();
       }
     }
   }
@@ -717,7 +767,7 @@ cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.nsplit, p.B * p.Hkv);
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(DecLayout<EXACT>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

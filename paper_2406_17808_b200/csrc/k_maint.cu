@@ -91,6 +91,31 @@ __global__ void head_homogenize_kernel(int B, int Hkv, int len, int mode, float*
   }
 }
 
+// Homogeneous policy with the median reduction (P:542 ablations): the median of every q-head's
+// mass (numpy's convention for an even count: the mean of the middle two), written to every
+// kv-head of the sequence.  Not a function of the per-kv-head reductions, so it reads the
+// per-q-head masses the score producer wrote to `heads`.
+__global__ void head_median_all_kernel(int B, int Hq, int Hkv, int len, const float* __restrict__ heads,
+                                       int heads_ld, float* __restrict__ s) {
+  const long long total = (long long)B * len;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / len;
+    const int x = (int)(i - b * len);
+    float hv[kMaxMedianGroup];
+    for (int h = 0; h < Hq; ++h) hv[h] = heads[(b * Hq + h) * (long long)heads_ld + x];
+    const float r = group_reduce_ablation(hv, Hq, 2);
+    for (int g = 0; g < Hkv; ++g) s[(b * Hkv + g) * (long long)len + x] = r;
+  }
+}
+
+void launch_head_median_all(int B, int Hq, int Hkv, int len, const float* heads, int heads_ld, float* s,
+                            cudaStream_t st) {
+  const long long total = (long long)B * len;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+  head_median_all_kernel<<<blocks, 256, 0, st>>>(B, Hq, Hkv, len, heads, heads_ld, s);
+}
+
 void launch_head_homogenize(int B, int Hkv, int len, int mode, float* s, cudaStream_t st) {
   const long long total = (long long)B * len;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);

@@ -68,6 +68,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 // 1D bulk copy global -> shared (bytes % 16 == 0, 16-B aligned), completion on `bar`.
+// L2 prefetch of a contiguous global range (bytes: multiple of 16, 16-B aligned source)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -245,8 +249,18 @@ __device__ __forceinline__ uint32_t elect_one() {
   return pred;
 }
 
+// bar.sync is barrier.sync.aligned: every thread of a participating warp must execute it
+// convergently, so the warp is reconverged first (a lane-0-only branch just before, e.g. an
+// mbarrier arrive, can leave it diverged; compute-sanitizer --tool synccheck flags that)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// Named barrier met at DIFFERENT instructions by different warp roles (e.g. a staging warp and
+// the math warps): the non-.aligned form, which allows that (bar.sync requires one instruction)
+__device__ __forceinline__ void named_bar_sync_roles(uint32_t id, uint32_t nthreads) {
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {

@@ -48,8 +48,8 @@ def test_config_validation(field, value, code):
 
 def test_ablation_options_validate():
     """head_reduce 0/1/2 (max, mean, median: P:542) and selection 0/1 (Q3) are accepted; others are
-    CONFIG errors; head_policy 0/1 (independent, homogeneous: P:542), except the median over all
-    heads of a sequence (UNSUPPORTED)."""
+    CONFIG errors; head_policy 0/1 (independent, homogeneous: P:542); the median over all heads of a
+    sequence needs Hq <= 32 (UNSUPPORTED above)."""
     import ctypes
     L = C.lib()
     assert C.validate(C.CascadeConfig(head_reduce="mean", selection=False)) == 0
@@ -58,7 +58,9 @@ def test_ablation_options_validate():
     assert C.validate(C.CascadeConfig(num_q_heads=32, num_kv_heads=2)) == -7      # bf16 group 16
     assert C.validate(C.CascadeConfig(num_q_heads=32, num_kv_heads=2, dtype="f32")) == 0
     assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="mean")) == 0
-    assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="median")) == -7
+    assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="median")) == 0
+    assert C.validate(C.CascadeConfig(head_policy="homogeneous", head_reduce="median", num_q_heads=64,
+                                      num_kv_heads=8)) == -7
     for field, value, code in [("head_reduce", 3, -2), ("selection", 2, -2), ("head_policy", 2, -2)]:
         st = C.CascadeConfig().c_struct()
         setattr(st, field, value)

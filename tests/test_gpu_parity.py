@@ -224,11 +224,13 @@ def test_decode_matches_oracle(Hq, exact_rope):
     ("bf16", "median", True, "independent"), ("f32", "median", True, "independent"),
     ("bf16", "max", False, "independent"),
     ("bf16", "max", True, "homogeneous"), ("f32", "max", True, "homogeneous"),
-    ("bf16", "mean", True, "homogeneous")])
+    ("bf16", "mean", True, "homogeneous"), ("bf16", "median", True, "homogeneous"),
+    ("f32", "median", True, "homogeneous")])
 def test_ablation_variants_end_to_end(dtype, head_reduce, selection, head_policy):
     """The paper's ablations through both prefill paths and decode: the mean and median head
-    reductions and the homogeneous head policy and no token selection (Q3),
-    GQA 4:1, B = 2, ragged last chunk."""
+    reductions and the homogeneous head policy (with the median: the median over all 8
+    q-heads of a sequence, from the per-head masses) and no token selection (Q3), GQA 4:1,
+    B = 2, ragged last chunk."""
     d = 128 if dtype == "bf16" else 64
     cfg = C.CascadeConfig(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=d, sink_size=4,
                           cache_size=64, num_cascades=4, max_stride=48, dtype=dtype,
