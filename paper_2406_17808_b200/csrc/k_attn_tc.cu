@@ -80,9 +80,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   uint64_t* s_full = bars + 6;       // [2]
   uint64_t* p_full = bars + 8;       // [2]
   uint64_t* q_full = bars + 10;
-  uint64_t* pv_done = bars + 11;
+  uint64_t* pv_done[2] = {bars + 11, bars + 14};   // PV of tiles j with j % 2 == i
   uint64_t* cs_done = bars + 12;     // [2] EST: column sums of tile j in TMEM buffer j % 2
-  uint64_t* o_done = bars + 14;      // every MMA of the CTA complete (O final)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -97,10 +96,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(kv_full + i, 1); tc::mbar_init(kv_empty + i, 1); }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
     tc::mbar_init(q_full, 4);
-    tc::mbar_init(pv_done, 1);
+    tc::mbar_init(pv_done[0], 1);
+    tc::mbar_init(pv_done[1], 1);
     tc::mbar_init(cs_done + 0, 1);
     tc::mbar_init(cs_done + 1, 1);
-    tc::mbar_init(o_done, 1);
     tc::fence_mbar_init();
   }
   if (EST) {                                            // B operand rows 2..15 stay zero
@@ -185,7 +184,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
           tc::mma_bf16_ts(tmem + kColO, pbase + kk * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         if (j + kStages < nt) tc::mma_commit(kv_empty + (j % kStages));   // the producer waits only these
-        tc::mma_commit(pv_done);
+        tc::mma_commit(pv_done[j & 1]);
         if (EST) {                                      // column sums sum_r a_r P[r, key]
           constexpr uint32_t idesc_cs = tc::idesc_bf16_f32(128, 16, 0, 1);   // A MN-major, B K-major
           const uint32_t pb = tc::smem_u32(sPb) + (j & 1) * 2 * kTileBytes;
@@ -207,7 +206,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         pv(j);
         if (j + 2 < nt) qk(j + 2);
       }
-      tc::mma_commit(o_done);                          // the epilogue's one wait
 #ifdef CASCADE_PASS1_TRACE
       if (g_p1_trace) {
         const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -347,7 +345,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         if (__any_sync(0xffffffffu, need)) {
           {
             P1_T0();
-            tc::mbar_wait(pv_done, (j - 1) & 1);
+            tc::mbar_wait(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
             P1_ACC(w_pv);
           }
           tc::tc_fence_after();
@@ -382,15 +380,21 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       }
       tc::tmem_wait_st();
       tc::tc_fence_before();
+      // observe PV(j-1) (long done by now: it only needed P(j-1)), so every pv_done phase has a
+      // waiter -- compute-sanitizer synccheck reports phases nobody waits for
+      if (j >= 1) tc::mbar_wait(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
       if (EST && j > 0) est_readout(j - 1);
     }
     if (EST && nt > 0) est_readout(nt - 1);
-    // epilogue: o_done is committed once, after the last MMA (a parity wait on pv_done could
-    // not tell PV(nt-1) done from PV(nt-3) done: with EST the cs_done wait above lets PV(nt-1)
-    // finish first, and a wait for phase nt-2 then blocks forever)
-    tc::mbar_wait(o_done, 0);
+    // epilogue: O final once PV(nt-1) is done.  One barrier per PV parity: when this thread last
+    // saw S(j) complete, QK(j) -- issued after PV(j-2) -- was done, so barrier j % 2 can only be
+    // in the phase of PV(j) or past it and the parity wait is unambiguous.  (A single pv_done
+    // could not tell PV(nt-1) done from PV(nt-3) done: with EST the cs_done wait above lets
+    // PV(nt-1) finish first, and a parity wait for phase nt-2 then blocked forever.)  Both
+    // barriers' phases are all waited (PV(j-1) at the end of tile j), none left unobserved.
+    tc::mbar_wait(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
 #ifdef CASCADE_PASS1_TRACE
     if (g_p1_trace && threadIdx.x == 128) {
       const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;

@@ -36,6 +36,9 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <type_traits>
 #include "tc_util.cuh"
 
@@ -69,11 +72,13 @@ template <bool EXACT> struct DecLayout {
   static constexpr int kRowBytes = EXACT ? 1024 : 512;      // a-row: [64 float2 hi | 64 float2 lo] or hi only
   static constexpr int kARows = kHiRows * kRowBytes;        // a-rows per K stage
   static constexpr int kLoTables = EXACT ? 2 : 1;
-  // sK | sV | sQ | sP | sA | sLo (| sLoL) | scalars + barriers; sO aliases sQ / sP after the tiles
+  // sK | sV | sQ | sP | sA | sLo (| sLoL) | tile records | scalars + barriers; sO aliases sQ / sP
+  // after the tiles
+  static constexpr int max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
   static constexpr size_t smem(int GM) {
     return (size_t)kKStages * kTileBytes32K + (size_t)kVStages * kTileBytes32K + 4096 + kPBuf * 4096 +
-           (size_t)kKStages * kARows + (size_t)kLoTables * kLoRows * kLoStride + 4 * 8 * 4 + 40 * 4 + 64 +
-           24 * 8 + 1024;
+           (size_t)kKStages * kARows + (size_t)kLoTables * kLoRows * kLoStride + (size_t)max_tiles(GM) * 8 +
+           4 * 8 * 4 + 40 * 4 + 64 + 24 * 8 + 1024;
   }
 };
 }  // namespace
@@ -97,6 +102,23 @@ int decode_fused_max_tiles(int GM) { return (int)((kTmemCols - kColLg) / GM); }
 // and its warp 0 applies the insertion.
 // Tile descriptor (int4, host): start slot, length, pe of key 0 (pe of key j = pe0 + j: the host
 // splits a tile where a full ring wraps past its oldest slot).
+// Optional per-CTA timeline (build with CASCADE_NVCC_EXTRA=-DCASCADE_DEC_TRACE; the default build
+// has none of it): globaltimer at CTA start, after the prologue, after the last tile's softmax,
+// after the mass / fold epilogue, at the end.  CASCADE_DEC_TRACE=n (env) dumps launch n.
+#ifdef CASCADE_DEC_TRACE
+__device__ unsigned long long* g_dec_trace = nullptr;
+#define DEC_MARK(k)                                                                              \
+  do {                                                                                            \
+    if (g_dec_trace) {                                                                            \
+      unsigned long long _t;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                      \
+      g_dec_trace[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = _t;               \
+    }                                                                                             \
+  } while (0)
+#else
+#define DEC_MARK(k)
+#endif
+
 template <int GM, bool EXACT>
 __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                               const __grid_constant__ CUtensorMap tm_v,
@@ -115,7 +137,8 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
   uint8_t* sA = sP + kPBuf * 4096;                                  // kKStages x the tile's a-rows (cos/sin(32a theta))
   uint8_t* sLo = sA + kKStages * Lay::kARows;               // 32 x kLoStride: cos/sin(b theta_i), fp32 hi parts
   uint8_t* sLoL = sLo + (EXACT ? kLoRows * kLoStride : 0);  // (EXACT) their fp32 lo parts
-  float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sLoL + kLoRows * kLoStride);   // [4][8]
+  int2* sTile = reinterpret_cast<int2*>(sLoL + kLoRows * kLoStride);   // (start, len) of this CTA's tiles
+  float (*sRed)[8] = reinterpret_cast<float (*)[8]>(sTile + Lay::max_tiles(GM));   // [4][8]
   float* sO = reinterpret_cast<float*>(sQ);                 // [GM][128] scaled partial O (after the tiles)
   float* sML = reinterpret_cast<float*>(sRed + 4);          // [0, 8) max, [8, 16) sum, [16, 24) lse2
   float* sCorr = sML + 24;                                  // [8]
@@ -141,6 +164,7 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
   const int per = (n_tiles + ns - 1) / ns;
   const int tbeg = split * per, tend = min(n_tiles, tbeg + per);
   const int nt = max(0, tend - tbeg);
+  if (tid == 0) DEC_MARK(0);
 
   if (tid == 0) {
     for (int i = 0; i < kKStages; ++i) { tc::mbar_init(kfull + i, 1); tc::mbar_init(kempty + i, 1); }
@@ -174,12 +198,17 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
     *reinterpret_cast<float2*>(sLo + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + ii];
     if (EXACT) *reinterpret_cast<float2*>(sLoL + rr * kLoStride + ii * 8) = p.tab_lo[rr * 2 * HALF + HALF + ii];
   }
+  for (int o = tid; o < nt; o += blockDim.x) {              // the epilogue's tile records
+    const int ti = tbeg + o;
+    sTile[o] = ti < p.n_tiles ? make_int2(p.dec_tiles[ti].x, p.dec_tiles[ti].y) : make_int2(p.S_tot, 1);
+  }
   for (int o = tid; o < kPBuf * 4096 / 16; o += blockDim.x) reinterpret_cast<uint4*>(sP)[o] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *sTmem, tO = tmem + 16;            // S^T buffers at columns 0 and 32
+  if (tid == 0) DEC_MARK(1);
 
   // per-tile geometry (same on every warp): start slot, length, pe of key 0
   auto tile_info = [&](int ti, int& start, int& len, int& pe0) {
@@ -497,7 +526,9 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) sRed[w4][h] = v;
     }
+    if (nt > 1) tc::mbar_wait(pv_done[(nt - 2) & 1], ((nt - 2) >> 1) & 1);   // every phase observed
     if (nt > 0) tc::mbar_wait(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);   // O^T holds every tile
+    if (t == 0) DEC_MARK(2);
     tc::tmem_wait_st();
     tc::named_bar_sync(1, 128);
     if (t < GM) {
@@ -522,12 +553,13 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
     sCorr[tid] = (sML[tid] == -INFINITY) ? 0.f : exp2f(sML[tid] - M) / L;   // this CTA's O weight
   }
   __syncthreads();
-  if (warp >= 4) {
-    constexpr int kWG = 1 + kRotWG;                          // warpgroups sharing the tiles
-    const int wg = (warp - 4) >> 2;
+  {
+    // every warp shares the tiles now (TMEM lanes 32 (warp % 4) .. + 31 are each warp's own)
+    constexpr int kWG = 2 + kRotWG;
+    const int wg = warp >> 2;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int t = (warp & 3) * 32 + lane;                    // key (or d) = TMEM lane
-    if (wg == 0) {                                           // scaled partial O^T -> sO (own smem)
+    if (wg == 1) {                                           // scaled partial O^T -> sO (own smem)
       float ov[16];
       tc::tmem_ld16(tO + lane_off, ov);
       tc::tmem_wait_ld();
@@ -541,8 +573,9 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
     double* mu = p.mu + (long long)bg * p.S_tot;
     float* s_out = p.s + (long long)bg * (p.S_tot + 1);
     // kU tiles per round: every TMEM load and mu load of the round is issued before the first
-    // use, so the tail streams instead of paying one load round trip per tile
-    constexpr int kU = 4;
+    // use (tile records in shared memory, mu prefetched into L2 with its K tile), so the tail pays
+    // one L2 round trip per round
+    constexpr int kU = GM >= 8 ? 4 : GM >= 4 ? 6 : 8;
     for (int j0 = wg; j0 < nt; j0 += kWG * kU) {
       uint32_t lgb[kU][GM];
       double m0[kU];
@@ -551,9 +584,10 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int j = j0 + kWG * u;
-        int start = 0, len = 0, pe0 = 0;
+        int start = 0, len = 0;
         if (j < nt) {
-          tile_info(tbeg + j, start, len, pe0);
+          const int2 tr = sTile[j];
+          start = tr.x; len = tr.y;
           tc::tmem_ld_n<GM>(tmem + lane_off + kColLg + (uint32_t)(GM * j), lgb[u]);
         }
         vk[u] = j < nt && t < len;
@@ -584,6 +618,7 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
       }
     }
   }
+  if (tid == 128) DEC_MARK(3);
   // ======== cluster exchange #2: every fold and every s visible; partial O staged ========
   __threadfence();
   tc::tc_fence_before();
@@ -664,6 +699,7 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
   tc::tc_fence_before();
   __syncthreads();
   tc::cluster_sync();
+  if (tid == 0) DEC_MARK(4);
   if (warp == 2) {
     tc::tc_fence_after();
     tc::tmem_dealloc<kTmemCols>(tmem);
@@ -777,7 +813,41 @@ cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tk, tv, p, pl, n_sel, phase_begin_dev, n_phase, out);
+#ifdef CASCADE_DEC_TRACE
+  static unsigned long long* trace = nullptr;
+  static int trace_at = -1, calls = 0;
+  const size_t ctas = (size_t)p.nsplit * p.B * p.Hkv;
+  if (trace_at < 0) {
+    const char* ev = std::getenv("CASCADE_DEC_TRACE");
+    trace_at = ev ? std::atoi(ev) : 0;
+    if (trace_at > 0) {
+      cudaMalloc(&trace, ctas * 8 * 8);
+      cudaMemcpyToSymbol(g_dec_trace, &trace, sizeof(trace));
+    }
+  }
+#endif
+  const cudaError_t rc = cudaLaunchKernelEx(&cfg, kern, tk, tv, p, pl, n_sel, phase_begin_dev, n_phase, out);
+#ifdef CASCADE_DEC_TRACE
+  if (trace_at > 0 && ++calls == trace_at) {
+    std::vector<unsigned long long> h(ctas * 8);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (size_t c = 0; c < ctas; ++c) { t0 = std::min(t0, h[c * 8]); t1 = std::max(t1, h[c * 8 + 4]); }
+    double pro = 0, tiles = 0, epi = 0, fin = 0;
+    for (size_t c = 0; c < ctas; ++c) {
+      pro += h[c * 8 + 1] - h[c * 8]; tiles += h[c * 8 + 2] - h[c * 8 + 1];
+      epi += h[c * 8 + 3] - h[c * 8 + 2]; fin += h[c * 8 + 4] - h[c * 8 + 3];
+    }
+    std::fprintf(stderr, "decode trace: %zu CTAs, span %.1f us; per CTA avg: prologue %.2f us, tiles %.2f us, "
+                 "mass+fold %.2f us, exchange+insert %.2f us\n", ctas, (t1 - t0) / 1e3, pro / ctas / 1e3,
+                 tiles / ctas / 1e3, epi / ctas / 1e3, fin / ctas / 1e3);
+    for (size_t c = 0; c < ctas; c += ctas / 16)
+      std::fprintf(stderr, "  cta %zu start %.1f tiles_end %.1f end %.1f us\n", c, (h[c * 8] - t0) / 1e3,
+                   (h[c * 8 + 2] - t0) / 1e3, (h[c * 8 + 4] - t0) / 1e3);
+  }
+#endif
+  return rc;
 }
 
 cudaError_t launch_decode_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel,
