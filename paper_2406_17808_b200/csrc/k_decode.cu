@@ -542,17 +542,23 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
   tc::cluster_sync();
   tc::tc_fence_after();
   if (tid < GM) {                                            // final log2-domain LSE of head tid
+    float mr[8], lr[8];                                      // every CTA's (max, sum): loads first
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < ns) { mr[r] = tc::ld_cluster_f32(sML + tid, (uint32_t)r); lr[r] = tc::ld_cluster_f32(sML + 8 + tid, (uint32_t)r); }
     float M = -INFINITY;
-    for (int r = 0; r < ns; ++r) M = fmaxf(M, tc::ld_cluster_f32(sML + tid, (uint32_t)r));
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < ns) M = fmaxf(M, mr[r]);
     float L = 0.f;
-    for (int r = 0; r < ns; ++r) {
-      const float mr = tc::ld_cluster_f32(sML + tid, (uint32_t)r);
-      if (mr != -INFINITY) L += tc::ld_cluster_f32(sML + 8 + tid, (uint32_t)r) * exp2f(mr - M);
-    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < ns && mr[r] != -INFINITY) L += lr[r] * exp2f(mr[r] - M);
     sML[16 + tid] = M + log2f(L);
     sCorr[tid] = (sML[tid] == -INFINITY) ? 0.f : exp2f(sML[tid] - M) / L;   // this CTA's O weight
   }
   __syncthreads();
+  if (tid == 0) DEC_MARK(5);
   {
     // every warp shares the tiles now (TMEM lanes 32 (warp % 4) .. + 31 are each warp's own)
     constexpr int kWG = 2 + kRotWG;
@@ -633,7 +639,15 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
         for (int r = 0; r < ns; ++r) o += tc::ld_cluster_f32(sO + h * 128 + d, (uint32_t)r);
         out[((long long)b * p.Hq + g * G + h) * D + d] = __float2bfloat16_rn(o);
       }
-    } else if (warp == 0 && p.update) {
+    }
+  }
+  // ======== #3: peers keep their shared memory until rank 0 has read it; then they may exit
+  //          while rank 0 applies the insertion (it needs only global memory: every CTA's fold
+  //          is visible since #2) ========
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  if (crank == 0 && warp == 0 && p.update) {
       // ---- Alg. 2's single insertion: selections (depth order), then moves deepest first ----
       double* mu = p.mu + (long long)bg * p.S_tot;
       const float* s_out = p.s + (long long)bg * (p.S_tot + 1);
@@ -693,12 +707,7 @@ __global__ void __launch_bounds__(DecLayout<EXACT>::kThreads, 1) decode_fused_ke
         }
         __syncwarp();
       }
-    }
   }
-  // ======== #3: peers keep their shared memory until rank 0 has read it ========
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::cluster_sync();
   if (tid == 0) DEC_MARK(4);
   if (warp == 2) {
     tc::tc_fence_after();
@@ -834,14 +843,14 @@ cudaError_t launch_fused(const DecodeParams& p, const PlanDev& pl, int32_t n_sel
     cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull, t1 = 0;
     for (size_t c = 0; c < ctas; ++c) { t0 = std::min(t0, h[c * 8]); t1 = std::max(t1, h[c * 8 + 4]); }
-    double pro = 0, tiles = 0, epi = 0, fin = 0;
+    double pro = 0, tiles = 0, lse = 0, epi = 0, fin = 0;
     for (size_t c = 0; c < ctas; ++c) {
       pro += h[c * 8 + 1] - h[c * 8]; tiles += h[c * 8 + 2] - h[c * 8 + 1];
-      epi += h[c * 8 + 3] - h[c * 8 + 2]; fin += h[c * 8 + 4] - h[c * 8 + 3];
+      lse += h[c * 8 + 5] - h[c * 8 + 2]; epi += h[c * 8 + 3] - h[c * 8 + 5]; fin += h[c * 8 + 4] - h[c * 8 + 3];
     }
     std::fprintf(stderr, "decode trace: %zu CTAs, span %.1f us; per CTA avg: prologue %.2f us, tiles %.2f us, "
-                 "mass+fold %.2f us, exchange+insert %.2f us\n", ctas, (t1 - t0) / 1e3, pro / ctas / 1e3,
-                 tiles / ctas / 1e3, epi / ctas / 1e3, fin / ctas / 1e3);
+                 "cluster wait + LSE %.2f us, mass+fold %.2f us, exchange+insert %.2f us\n", ctas, (t1 - t0) / 1e3,
+                 pro / ctas / 1e3, tiles / ctas / 1e3, lse / ctas / 1e3, epi / ctas / 1e3, fin / ctas / 1e3);
     for (size_t c = 0; c < ctas; c += ctas / 16)
       std::fprintf(stderr, "  cta %zu start %.1f tiles_end %.1f end %.1f us\n", c, (h[c * 8] - t0) / 1e3,
                    (h[c * 8 + 2] - t0) / 1e3, (h[c * 8 + 4] - t0) / 1e3);
