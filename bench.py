@@ -398,6 +398,7 @@ def main():
     ap.add_argument("--score-mode", default="exact", choices=["exact", "onepass"],
                     help="per-key mass: exact two-pass (default) or the paper's one-pass estimator")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-onepass", action="store_true", help="skip the one-pass estimator line")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -644,6 +645,35 @@ def main():
                          "api": "cascade_prefill_stride_host_async + cascade_host_wait (pinned host q/k/v/out; "
                                 "copies on library streams, overlapped with compute; layers in call order)"}
         del Qh, Kh, Vh, Oh
+
+    # ---- the paper's one-pass estimator on the same inputs: another handle,
+    # its own warm-up, the same timed-step definition; reported beside the exact-mass headline ----
+    if not args.no_onepass and not use_dist and args.score_mode == "exact" and L == 1:
+        log("one-pass start")
+        cfg1 = C.CascadeConfig(**{**cfg.__dict__, "score_mode": "onepass"})
+        cas1 = C.Cascade(cfg1, device=local)
+        Q, K, V = sets[0]
+
+        def step1():
+            cas1.reset(0)
+            for c in range(nchunks):
+                cas1.prefill_stride(0, Q[c], K[c], V[c], out=outs[0][c % R])
+
+        for _ in range(3):
+            step1()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            step1()
+        g1.record()
+        torch.cuda.synchronize()
+        oms = g0.elapsed_time(g1) / args.steps
+        result["onepass"] = {"value": T * B / (oms / 1e3), "unit": "tok/s", "ms_per_step": oms,
+                             "score_mode": "onepass (Alg. 3 normaliser l + l rho / gamma, P:646; no pass 2)",
+                             "note": "the paper's estimator instead of the exact two-pass mass (reading Q6); same "
+                                     "inputs and step; DESIGN.md section 6b for its deviation from the exact mass"}
+        cas1.close()
 
     del sets, outs, gath
     cas.close()
