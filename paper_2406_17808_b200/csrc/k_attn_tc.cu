@@ -26,6 +26,14 @@
 #include <vector>
 #include <cstdio>
 
+// exp2 pairs of every 16 evaluated on the FMA pipe (the rest on MUFU): pass 1 and pass 2
+#ifndef CASCADE_FWD_EMU
+#define CASCADE_FWD_EMU 4
+#endif
+#ifndef CASCADE_SCORE_EMU
+#define CASCADE_SCORE_EMU 4
+#endif
+
 namespace cascade {
 
 namespace {
@@ -696,7 +704,7 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
     if (d == 128) go(attn_fwd_tc_kernel<128, 4, true>);
     else go(attn_fwd_tc_kernel<64, 4, true>);
   } else {
-    if (d == 128) go(attn_fwd_tc_kernel<128, 4, false>);
+    if (d == 128) go(attn_fwd_tc_kernel<128, CASCADE_FWD_EMU, false>);
     else go(attn_fwd_tc_kernel<64, 4, false>);
   }
 #ifdef CASCADE_PASS1_TRACE
@@ -727,9 +735,9 @@ void launch_attn_score_tc(const TcParams& p, const CUtensorMap& tq, const CUtens
     kern<<<grid, 640, smem, st>>>(tq, tk, p);
   };
   if (d == 128) {
-    go(attn_score_tc_kernel<128, 4, 3>);
+    go(attn_score_tc_kernel<128, CASCADE_SCORE_EMU, 3>);
   } else {
-    go(attn_score_tc_kernel<64, 4, 3>);
+    go(attn_score_tc_kernel<64, CASCADE_SCORE_EMU, 3>);
   }
 }
 
