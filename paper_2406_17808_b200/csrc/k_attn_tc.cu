@@ -25,7 +25,6 @@
 #include <type_traits>
 #include <vector>
 #include <cstdio>
-#include <cstdlib>
 
 // exp2 pairs of every 16 evaluated on the FMA pipe (the rest on MUFU): pass 1 and pass 2
 #ifndef CASCADE_FWD_EMU
@@ -670,305 +669,6 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
   }
 }
 
-// Pass 1, key-split variant (CASCADE_PASS1_SPLIT=1 selects it at run time; exact mass only).
-// The baseline's softmax is one warp per SM sub-partition and is the critical path (DESIGN.md
-// 8b).  Here every row's 128 keys of a tile are split between two softmax warps of the same
-// sub-partition (TMEM lanes are per sub-partition, so the halves split columns, not rows): half A
-// owns keys 0-63, half B keys 64-127, and each half keeps its OWN running max, row sum and
-// output accumulator (O_A, O_B in TMEM), so the halves never synchronise inside the tile loop;
-// they are merged once at the end (m = max(mA, mB), O = (O_A 2^(mA-m) + O_B 2^(mB-m)) / l).
-// TMEM: S0 [0,128), S1 [128,256), O_A [256, 256+D), O_B [256+D, 256+2D) -- full, so Q moves to
-// shared memory and QK^T is an SS MMA (one more 32 KB shared-memory read per tile).  Each half
-// writes its bf16 P into the S columns it has already read (A: [0,32), B: [64,96) of the buffer)
-// and PV_A / PV_B read them as TMEM A operands against key rows 0-63 / 64-127 of the V tile.
-// Warps: 0 K producer (+ Q), 1 MMA issuer, 2 TMEM allocator, 3 V producer, 4-7 softmax A,
-// 8-11 softmax B.  K ring (3 stages) freed by QK, V ring (3 stages) freed by both PVs.
-template <int D, int EMU>
-__global__ void __launch_bounds__(384, 1)
-attn_fwd_split_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_vs, const __grid_constant__ CUtensorMap tm_vc,
-                      TcParams p) {
-  constexpr int KB = D / 64;
-  constexpr int kKS = 3, kVS = 3;
-  constexpr uint32_t kColOA = 256, kColOB = 256 + D;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sQ = smem;                                   // KB blocks (A operand of QK^T)
-  uint8_t* sK = sQ + KB * kTileBytes;                   // kKS x KB blocks
-  uint8_t* sV = sK + kKS * KB * kTileBytes;             // kVS x KB blocks
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVS * KB * kTileBytes);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;        // [3]
-  uint64_t* k_empty = bars + 4;       // [3]
-  uint64_t* v_full = bars + 7;        // [3]
-  uint64_t* v_empty = bars + 10;      // [3]
-  uint64_t* s_full = bars + 13;       // [2]
-  uint64_t* ph_full = bars + 15;      // [2 halves][2]: P of half h, S buffer parity
-  uint64_t* pv_done = bars + 19;      // [2 halves][2]: PV_h of tiles j with j % 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 23);
-  float* sML = reinterpret_cast<float*>(sQ);            // [2 halves][2 (m, l)][128], after the last QK
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * 128;
-  const int gkv = h / p.G;
-  const long long bg = (long long)b * p.Hkv + gkv;
-  const int n_chunk_tiles = min(q0 / 128 + 1, (p.m + 127) / 128);
-  const int nt = p.n_res_tiles + n_chunk_tiles;
-
-  if (threadIdx.x == 0) {
-    tc::mbar_init(q_full, 1);
-    for (int i = 0; i < kKS; ++i) { tc::mbar_init(k_full + i, 1); tc::mbar_init(k_empty + i, 1); }
-    for (int i = 0; i < kVS; ++i) { tc::mbar_init(v_full + i, 1); tc::mbar_init(v_empty + i, 1); }
-    for (int i = 0; i < 2; ++i) tc::mbar_init(s_full + i, 1);
-    for (int i = 0; i < 4; ++i) { tc::mbar_init(ph_full + i, 4); tc::mbar_init(pv_done + i, 1); }
-    tc::fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&tm_q); tc::tma_prefetch(&tm_k); tc::tma_prefetch(&tm_vs); tc::tma_prefetch(&tm_vc);
-  }
-  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  auto tile_rows = [&](int j, int& krow, int& vrow, const CUtensorMap*& vm) {
-    if (j < p.n_res_tiles) {
-      const int2 t = p.res_tiles[j];
-      krow = (int)(bg * (p.S_tot + p.M) + t.x);
-      vrow = (int)(bg * p.S_tot + t.x);
-      vm = &tm_vs;
-    } else {
-      const int k0 = (j - p.n_res_tiles) * 128;
-      krow = (int)(bg * (p.S_tot + p.M) + p.S_tot + k0);
-      vrow = (int)(bg * p.M + k0);
-      vm = &tm_vc;
-    }
-  };
-
-  if (warp == 0) {
-    // ---------------- TMA: the Q tile once, then K tiles ----------------
-    if (tc::elect_one()) {
-      const int qrow = (int)(((long long)b * p.Hq + h) * p.M + q0);
-      tc::mbar_expect_tx(q_full, KB * kTileBytes);
-      for (int kb = 0; kb < KB; ++kb) tc::tma_load_2d(sQ + kb * kTileBytes, &tm_q, q_full, kb * 64, qrow);
-      for (int j = 0; j < nt; ++j) {
-        const int s = j % kKS;
-        if (j >= kKS) tc::mbar_wait(k_empty + s, ((j / kKS) - 1) & 1);
-        int krow, vrow;
-        const CUtensorMap* vm;
-        tile_rows(j, krow, vrow, vm);
-        tc::mbar_expect_tx(k_full + s, KB * kTileBytes);
-        for (int kb = 0; kb < KB; ++kb)
-          tc::tma_load_2d(sK + (s * KB + kb) * kTileBytes, &tm_k, k_full + s, kb * 64, krow);
-      }
-    }
-  } else if (warp == 3) {
-    // ---------------- TMA: V tiles ----------------
-    if (tc::elect_one()) {
-      for (int j = 0; j < nt; ++j) {
-        const int s = j % kVS;
-        if (j >= kVS) tc::mbar_wait(v_empty + s, ((j / kVS) - 1) & 1);
-        int krow, vrow;
-        const CUtensorMap* vm;
-        tile_rows(j, krow, vrow, vm);
-        tc::mbar_expect_tx(v_full + s, KB * kTileBytes);
-        for (int kb = 0; kb < KB; ++kb)
-          tc::tma_load_2d(sV + (s * KB + kb) * kTileBytes, vm, v_full + s, kb * 64, vrow);
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (tc::elect_one()) {
-      constexpr uint32_t idesc_qk = tc::idesc_bf16_f32(128, 128, 0);
-      constexpr uint32_t idesc_pv = tc::idesc_bf16_f32(128, D, 1);
-      const uint32_t aQ = tc::smem_u32(sQ), aK = tc::smem_u32(sK), aV = tc::smem_u32(sV);
-      auto qk = [&](int j) {
-        const int s = j % kKS;
-        tc::mbar_wait(k_full + s, (j / kKS) & 1);
-        tc::tc_fence_after();
-        const uint32_t kbase = aK + s * KB * kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = tc::desc_kmajor_sw128(aQ + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          const uint64_t db = tc::desc_kmajor_sw128(kbase + (kk >> 2) * kTileBytes + (kk & 3) * 32);
-          tc::mma_bf16_ss(tmem + (j & 1) * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
-        }
-        if (j + kKS < nt) tc::mma_commit(k_empty + s);   // the producer waits only these
-        tc::mma_commit(s_full + (j & 1));
-      };
-      auto pv = [&](int j, int half) {
-        tc::mbar_wait(ph_full + half * 2 + (j & 1), (j >> 1) & 1);
-        tc::tc_fence_after();
-        const uint32_t vbase = aV + (j % kVS) * KB * kTileBytes;
-        const uint32_t pbase = tmem + (j & 1) * 128 + half * 64;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {             // this half's 64 keys = 4 x K16
-          const uint64_t db = tc::desc_mnmajor_sw128(vbase + (half * 4 + kk) * 2048, kTileBytes);
-          tc::mma_bf16_ts(tmem + (half ? kColOB : kColOA), pbase + kk * 8, db, idesc_pv,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(pv_done + half * 2 + (j & 1));
-      };
-      tc::mbar_wait(q_full, 0);
-      qk(0);
-      if (nt > 1) qk(1);
-      for (int j = 0; j < nt; ++j) {
-        tc::mbar_wait(v_full + (j % kVS), (j / kVS) & 1);
-        pv(j, 0);
-        pv(j, 1);
-        if (j + kVS < nt) tc::mma_commit(v_empty + (j % kVS));
-        if (j + 2 < nt) qk(j + 2);
-      }
-    }
-  } else if (warp >= 4) {
-    // ---------------- softmax: half A (warps 4-7) or B (warps 8-11) ----------------
-    const int half = (warp - 4) >> 2;
-    const int r = (warp & 3) * 32 + lane;                 // query row = TMEM lane
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t cO = half ? kColOB : kColOA;
-    const int qi = q0 + r;
-    float m_used = -INFINITY, l = 0.f;
-    float x[64];
-    for (int j = 0; j < nt; ++j) {
-      const uint32_t sb = tmem + (j & 1) * 128 + half * 64 + lane_off;
-      tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
-      tc::tc_fence_after();
-      tc::tmem_ld32(sb, x);
-      tc::tmem_ld32(sb + 32, x + 32);
-      tc::tmem_wait_ld();
-      int lim;                                            // keys [0, lim) of the tile are visible
-      if (j < p.n_res_tiles) {
-        lim = p.res_tiles[j].y;
-      } else {
-        const int k0 = (j - p.n_res_tiles) * 128;
-        lim = min(qi - k0 + 1, p.m - k0);
-      }
-      lim -= half * 64;                                   // in this half's key index
-      if (lim < 64) {
-#pragma unroll
-        for (int c = 0; c < 64; ++c) x[c] = c < lim ? x[c] : -INFINITY;
-      }
-      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-      auto exp_pass = [&](float mu, float& mraw, auto track) -> float {
-        const float2 nm2 = make_float2(-mu, -mu);
-        float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-        float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {                     // 32 keys -> 16 packed columns per store
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float xa = x[c * 32 + 2 * e], xb = x[c * 32 + 2 * e + 1];
-            if (decltype(track)::value) { m0 = fmaxf(m0, xa); m1 = fmaxf(m1, xb); }
-            const float2 t = __ffma2_rn(make_float2(xa, xb), sc2, nm2);
-            const bool emu = ((e * EMU) % 16) + EMU >= 16;
-            const float2 pp = emu ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
-            if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
-            pk[e] = tc::pack_bf16(pp.x, pp.y);
-          }
-          // P of this half into the S columns it has read: [0, 32) (A) or [64, 96) (B)
-          tc::tmem_st16(tmem + (j & 1) * 128 + half * 64 + lane_off + c * 16, pk);
-        }
-        if (decltype(track)::value) mraw = fmaxf(m0, m1);
-        const float2 s01 = __fadd2_rn(s0, s1);
-        return s01.x + s01.y;
-      };
-      using Track = std::integral_constant<bool, true>;
-      using NoTrack = std::integral_constant<bool, false>;
-      float mraw = -INFINITY;
-      if (j == 0) {
-        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 64; c += 4) {
-          m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
-        }
-        m_used = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * p.scale_log2;
-        l += exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, NoTrack{});
-      } else {
-        // exp2 against this half's running max right away; only if the tile max grew by more
-        // than 2^8 (rare) is this half's O rescaled (after PV_h(j-1)) and the tile redone
-        const float sum = exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, Track{});
-        const float mx = mraw * p.scale_log2;
-        const bool need = mx > m_used + 8.f;
-        if (__any_sync(0xffffffffu, need)) {
-          tc::mbar_wait(pv_done + half * 2 + ((j - 1) & 1), ((j - 1) >> 1) & 1);
-          tc::tc_fence_after();
-          const float f = need ? tc::fast_exp2(m_used - mx) : 1.f;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            tc::tmem_ld32(tmem + cO + lane_off + c * 32, o);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= f;
-            tc::tmem_st32(tmem + cO + lane_off + c * 32, o);
-          }
-          if (need) { l *= f; m_used = mx; }
-          tc::tmem_wait_st();
-          l += exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, NoTrack{});
-        } else {
-          l += sum;
-        }
-      }
-      tc::tmem_wait_st();
-      tc::tc_fence_before();
-      if (j >= 1) tc::mbar_wait(pv_done + half * 2 + ((j - 1) & 1), ((j - 1) >> 1) & 1);   // every phase observed
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ph_full + half * 2 + (j & 1));
-    }
-    tc::mbar_wait(pv_done + half * 2 + ((nt - 1) & 1), ((nt - 1) >> 1) & 1);   // O_h final
-    tc::tc_fence_after();
-    // ---- merge the halves (once): (m, l) through shared memory (Q's, no longer read) ----
-    sML[(half * 2 + 0) * 128 + r] = m_used;
-    sML[(half * 2 + 1) * 128 + r] = l;
-    tc::named_bar_sync_roles(1, 256);
-    const float mA = sML[0 * 128 + r], lA = sML[1 * 128 + r];
-    const float mB = sML[2 * 128 + r], lB = sML[3 * 128 + r];
-    const float mm = fmaxf(mA, mB);
-    const float fA = mA == -INFINITY ? 0.f : tc::fast_exp2(mA - mm);
-    const float fB = mB == -INFINITY ? 0.f : tc::fast_exp2(mB - mm);
-    const float lt = lA * fA + lB * fB;
-    const float inv = 1.f / lt;
-    const bool store = qi < p.m;
-    __nv_bfloat16* orow = p.out + (((long long)b * p.m + qi) * p.Hq + h) * D;
-    // each half stores half of the head dimension: columns [half D/2, half D/2 + D/2)
-#pragma unroll
-    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
-      float oa[32], ob[32];
-      tc::tmem_ld32(tmem + kColOA + lane_off + c * 32, oa);
-      tc::tmem_ld32(tmem + kColOB + lane_off + c * 32, ob);
-      tc::tmem_wait_ld();
-      if (store) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          float w[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) w[e] = (oa[8 * v + e] * fA + ob[8 * v + e] * fB) * inv;
-          dst[v] = make_uint4(tc::pack_bf16(w[0], w[1]), tc::pack_bf16(w[2], w[3]), tc::pack_bf16(w[4], w[5]),
-                              tc::pack_bf16(w[6], w[7]));
-        }
-      }
-    }
-    // pass-2 bias per query row: lse2 - log2(w_r); +inf for rows past m (they weigh nothing)
-    if (half == 0)
-      p.qbias[((long long)b * p.Hq + h) * p.Mb + qi] = store ? mm + log2f(lt) - p.log2w[qi] : INFINITY;
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc<512>(tmem);
-  }
-}
-
-size_t attn_fwd_split_smem(int d) {
-  const int KB = d / 64;
-  return 1024 + (size_t)(KB + 3 * KB + 3 * KB) * kTileBytes + 24 * 8 + 16;
-}
-
 size_t attn_fwd_tc_smem(int d, bool est) {
   const int KB = d / 64;
   return est ? 1024 + (size_t)(2 * 2 * KB) * kTileBytes + 2 * 2 * kTileBytes + 2 * 4096 + 16 * 8 + 64
@@ -978,15 +678,6 @@ size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
   return 1024 + (size_t)(2 * KB + 4 * KB) * kTileBytes + 4 * 128 * 4 + (size_t)4 * G * 128 * 4 + 16 * 8 + 64 +
          2 * 128 * 8;
-}
-
-static bool pass1_split() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("CASCADE_PASS1_SPLIT");
-    v = (e && std::atoi(e) > 0) ? 1 : 0;
-  }
-  return v == 1;
 }
 
 void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -1012,14 +703,6 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
   if (est) {
     if (d == 128) go(attn_fwd_tc_kernel<128, 4, true>);
     else go(attn_fwd_tc_kernel<64, 4, true>);
-  } else if (pass1_split()) {              // CASCADE_PASS1_SPLIT=1: the key-split variant
-    const size_t sm2 = attn_fwd_split_smem(d);
-    auto go2 = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      kern<<<grid, 384, sm2, st>>>(tq, tk, tvs, tvc, p);
-    };
-    if (d == 128) go2(attn_fwd_split_kernel<128, CASCADE_FWD_EMU>);
-    else go2(attn_fwd_split_kernel<64, 4>);
   } else {
     if (d == 128) go(attn_fwd_tc_kernel<128, CASCADE_FWD_EMU, false>);
     else go(attn_fwd_tc_kernel<64, 4, false>);
