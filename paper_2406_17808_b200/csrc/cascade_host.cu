@@ -2,6 +2,7 @@
 // mirror, schedule upload and the launch sequence of each call.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -188,6 +189,7 @@ struct cascade_handle {
   bool poisoned;
   // profiling (cascade_profile_*)
   bool profiling;
+  bool nvtx;                 // CASCADE_NVTX=1: an NVTX range per launch group (ncu --nvtx, nsys)
   struct Rec { cudaEvent_t a, b; double work; };
   std::vector<Rec> recs[CASCADE_PROFILE_CLASSES];
   std::vector<cudaEvent_t> ev_pool;
@@ -209,9 +211,16 @@ cudaEvent_t pool_event(cascade_handle* h) {
 
 // RAII-ish scope: records a start event on construction and an end event on finish().
 struct ProfScope {
-  cascade_handle* h; int cls; cudaStream_t st; cudaEvent_t a = nullptr;
+  cascade_handle* h; int cls; cudaStream_t st; cudaEvent_t a = nullptr; bool pushed = false;
   ProfScope(cascade_handle* h_, int cls_, cudaStream_t st_) : h(h_), cls(cls_), st(st_) {
+    static const char* const kNames[CASCADE_PROFILE_CLASSES] = {"cascade.prep", "cascade.attn_fwd",
+                                                                "cascade.attn_score", "cascade.maintenance",
+                                                                "cascade.decode"};
+    if (h->nvtx) { nvtxRangePushA(kNames[cls]); pushed = true; }
     if (h->profiling) { a = pool_event(h); cudaEventRecord(a, st); }
+  }
+  ~ProfScope() {
+    if (pushed) nvtxRangePop();
   }
   void finish(double work) {
     if (!a) return;
@@ -336,6 +345,10 @@ cascade_status cascade_init(const cascade_config* cfg, void* d_ws, size_t ws_byt
   h->poisoned = false;
   h->ring_pos = 0;
   h->profiling = false;
+  {
+    const char* e = std::getenv("CASCADE_NVTX");
+    h->nvtx = e && std::atoi(e) > 0;
+  }
   h->moved_seen = 0;
   h->moved_chunk = 0;
   for (int i = 0; i < kRing; ++i) { h->pinned[i] = nullptr; h->ring_ev[i] = nullptr; }

@@ -251,7 +251,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     float x[128];
     // EST: tile jj's column sums (lane = key) -> s_heads[b][h][key] (atomic: every q-tile adds)
     auto est_readout = [&](int jj) {
-      tc::mbar_wait(cs_done + (jj & 1), (jj >> 1) & 1);
+      tc::mbar_wait_unbounded(cs_done + (jj & 1), (jj >> 1) & 1);
       tc::tc_fence_after();
       uint32_t cv[2];
       tc::tmem_ld_n<2>(tmem + kColCs + (jj & 1) * 16 + lane_off, cv);
@@ -274,7 +274,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       const uint32_t sb = tmem + (j & 1) * 128 + lane_off;
       {
         P1_T0();
-        tc::mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+        tc::mbar_wait_unbounded(s_full + (j & 1), (j >> 1) & 1);
         P1_ACC(w_s);
       }
       tc::tc_fence_after();
@@ -353,7 +353,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         if (__any_sync(0xffffffffu, need)) {
           {
             P1_T0();
-            tc::mbar_wait(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+            tc::mbar_wait_unbounded(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
             P1_ACC(w_pv);
           }
           tc::tc_fence_after();
@@ -390,7 +390,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       tc::tc_fence_before();
       // observe PV(j-1) (long done by now: it only needed P(j-1)), so every pv_done phase has a
       // waiter -- compute-sanitizer synccheck reports phases nobody waits for
-      if (j >= 1) tc::mbar_wait(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+      if (j >= 1) tc::mbar_wait_unbounded(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
       if (EST && j > 0) est_readout(j - 1);
@@ -402,7 +402,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     // could not tell PV(nt-1) done from PV(nt-3) done: with EST the cs_done wait above lets
     // PV(nt-1) finish first, and a parity wait for phase nt-2 then blocked forever.)  Both
     // barriers' phases are all waited (PV(j-1) at the end of tile j), none left unobserved.
-    tc::mbar_wait(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
+    tc::mbar_wait_unbounded(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
 #ifdef CASCADE_PASS1_TRACE
     if (g_p1_trace && threadIdx.x == 128) {
       const long long cta = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;

@@ -49,8 +49,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// A wait that cannot complete (a phase nobody will ever arrive on -- the bug class of the
+// round-2 one-pass hang) traps after kHangNs instead of hanging the device: the launch then
+// fails with an error the host sees.  The fast path (phase already complete) is one try_wait.
+constexpr unsigned long long kHangNs = 20000000000ull;   // 20 s
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Unbounded form for code at the register limit (pass 1's softmax warps, 255 registers: the
+// timer of the bounded form costs spills there); a hang still traps through the bounded waits of
+// the CTA's other roles.
+__device__ __forceinline__ void mbar_wait_unbounded(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (!mbar_try_wait(bar, parity)) {
+    if (globaltimer_ns() - t0 > kHangNs) __trap();
   }
 }
 
