@@ -10,9 +10,10 @@ from paper_2406_17808_b200.synth import Synth
 fill = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 timed = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 m = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
+mode = sys.argv[4] if len(sys.argv) > 4 else "exact"      # or "onepass"
 peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["bf16_tflops"]
 cfg = C.CascadeConfig(batch=1, num_q_heads=32, num_kv_heads=8, head_dim=128, sink_size=64, cache_size=65536,
-                      num_cascades=8, max_stride=m, dtype="bf16")
+                      num_cascades=8, max_stride=m, dtype="bf16", score_mode=mode)
 cas = C.Cascade(cfg)
 syn = Synth(1, 32, 8, 128, seed=11)
 g = torch.Generator(device="cuda").manual_seed(1)
