@@ -40,7 +40,8 @@
  * Memory: the caller owns every device buffer.  The library never calls
  * cudaMalloc; it carves the caller's workspace (cascade_workspace_bytes) and
  * allocates only a small pinned host ring for schedule uploads.  All device
- * pointers must be on `device`, contiguous, 16-byte aligned.
+ * pointers must be on `device`, contiguous, 16-byte aligned (a misaligned I/O
+ * pointer is INVALID_ARG, checked before anything is launched).
  *
  * Ordering: calls on one layer must be issued in order on one stream (the
  * handle keeps a host mirror of the cascade counters so no call needs a

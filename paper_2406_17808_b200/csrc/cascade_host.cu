@@ -622,6 +622,9 @@ uint64_t moved_total(cascade_handle* h) {
   return tot;
 }
 
+// device I/O pointers are read / written with 16-byte vectors and TMA (cascade.h: 16-B aligned)
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 // row stride of the per-q-head mass buffers (s_heads, s_allheads): S_tot + max_stride rounded to 128
 inline int heads_ld(const cascade_handle* h) { return h->S_tot + (h->cfg.max_stride + 127) / 128 * 128; }
 
@@ -905,7 +908,7 @@ cascade_status cascade_prefill_stride(cascade_handle* h, int32_t layer, const vo
                                       const void* v, int32_t m, void* out, void* stream) {
   cascade_status rc = check_call(h, layer, m);
   if (rc != CASCADE_OK) return rc;
-  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  if (!q || !k || !v || !out || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out)) return CASCADE_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (h->cfg.dtype == CASCADE_BF16)
     return prefill_impl<__nv_bfloat16>(h, layer, static_cast<const __nv_bfloat16*>(q),
@@ -988,7 +991,7 @@ cascade_status cascade_decode(cascade_handle* h, int32_t layer, const void* q, c
   if (h == nullptr || !fused_decode_eligible(h)) return cascade_prefill_stride(h, layer, q, k, v, 1, out, stream);
   cascade_status rc = check_call(h, layer, 1);
   if (rc != CASCADE_OK) return rc;
-  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  if (!q || !k || !v || !out || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out)) return CASCADE_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const auto* kb = static_cast<const __nv_bfloat16*>(k);
   const auto* vb = static_cast<const __nv_bfloat16*>(v);
@@ -1004,7 +1007,7 @@ cascade_status cascade_attend(cascade_handle* h, int32_t layer, const void* q, c
                               int32_t m, void* out, void* stream) {
   cascade_status rc = check_call(h, layer, m);
   if (rc != CASCADE_OK) return rc;
-  if (!q || !k || !v || !out) return CASCADE_ERR_INVALID_ARG;
+  if (!q || !k || !v || !out || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out)) return CASCADE_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Pending& pd = h->pending[layer];
   if (m == 1 && fused_decode_eligible(h)) {
@@ -1031,7 +1034,7 @@ cascade_status cascade_score_buffer(cascade_handle* h, int32_t layer, float** s,
 }
 
 cascade_status cascade_commit(cascade_handle* h, int32_t layer, const void* k, const void* v, void* stream) {
-  if (!h || !k || !v || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
+  if (!h || !k || !v || !aligned16(k) || !aligned16(v) || layer < 0 || layer >= h->cfg.num_layers) return CASCADE_ERR_INVALID_ARG;
   if (h->poisoned) return CASCADE_ERR_POISONED;
   (void)cudaGetLastError();
   Pending& pd = h->pending[layer];
@@ -1049,7 +1052,7 @@ cascade_status cascade_update_with_scores(cascade_handle* h, int32_t layer, cons
                                           const void* v, int32_t m, const float* s, void* stream) {
   cascade_status rc = check_call(h, layer, m);
   if (rc != CASCADE_OK) return rc;
-  if (!k || !v || !s) return CASCADE_ERR_INVALID_ARG;
+  if (!k || !v || !s || !aligned16(k) || !aligned16(v) || !aligned16(s)) return CASCADE_ERR_INVALID_ARG;
   // the median of all q-heads (homogeneous + median) is not a function of per-kv-head s
   if (h->cfg.head_policy == 1 && h->cfg.head_reduce == 2) return CASCADE_ERR_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -120,3 +120,25 @@ def test_load_state_round_trip():
     bad["counts"] = [3] + list(snap["counts"][1:])
     with pytest.raises(C.CascadeError):
         b.load_state(0, bad)
+
+
+def test_misaligned_pointers_rejected_before_any_launch():
+    """cascade.h: device I/O pointers must be 16-byte aligned (vector loads, TMA); a misaligned one
+    is INVALID_ARG from the host check, with nothing launched and the mirror unchanged."""
+    import ctypes
+    cfg = _cfg(num_layers=1)
+    cas = C.Cascade(cfg)
+    syn = Synth(2, 16, 4, 128, seed=3)
+    q, k, v = (t.cuda() for t in syn.chunk(0, 16))
+    out = torch.empty_like(q)
+    n0 = cas.launch_count()
+    L = C.lib()
+    bad = ctypes.c_void_p(q.data_ptr() + 2)
+    rc = L.cascade_prefill_stride(cas._h, 0, bad, C._ptr(k), C._ptr(v), 16, C._ptr(out), C._stream(None))
+    assert rc == -1
+    rc = L.cascade_decode(cas._h, 0, C._ptr(q), ctypes.c_void_p(k.data_ptr() + 8), C._ptr(v), C._ptr(out),
+                          C._stream(None))
+    assert rc == -1
+    assert cas.launch_count() == n0 and cas.state(0)["t"] == 0
+    cas.prefill_stride(0, q, k, v)                      # the handle still works
+    assert cas.state(0)["t"] == 16
