@@ -79,6 +79,8 @@ void run(const char* name, int sms) {
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<16, false>("M128 N16  SS", sms);
+  run<32, false>("M128 N32  SS", sms);
   run<64, false>("M128 N64  SS", sms);
   run<128, false>("M128 N128 SS", sms);
   run<256, false>("M128 N256 SS", sms);
