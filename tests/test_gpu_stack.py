@@ -182,3 +182,21 @@ def test_stack_rejects_bad_inputs():
         st.prefill(torch.zeros((B, 10, D_MODEL + 1), dtype=torch.bfloat16, device="cuda"), 8)
     with pytest.raises(C.CascadeError):
         st.prefill(torch.zeros((B, 10, D_MODEL), dtype=torch.bfloat16, device="cuda"), cfg.max_stride + 1)
+
+
+def test_stack_host_buffers_and_ragged_length_match_device_run():
+    """x / y in pinned host memory (the chunk gather / scatter are 2-D host<->device copies inside
+    the library) and a length that is not a multiple of the stride: bit-identical to the run on
+    device buffers."""
+    cfg = _cfg()
+    ws, rng = _weights(5)
+    T, m = 77, 32
+    x = _bf(rng.standard_normal((B, T, D_MODEL)))
+    _, st_d = _stack(cfg, ws)
+    y_dev = st_d.prefill(x.cuda(), m)
+    _, st_h = _stack(cfg, ws)
+    xh = x.pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    st_h.prefill(xh, m, yh)
+    torch.cuda.synchronize()
+    assert torch.equal(yh.view(torch.int16), y_dev.cpu().view(torch.int16))
