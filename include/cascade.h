@@ -309,7 +309,11 @@ void cascade_stack_destroy(cascade_stack* s);
  * in ceil(T/m) chunks of m <= max_stride tokens (the last may be ragged).  All work
  * is enqueued before returning; `stream` waits for the last chunk's last layer
  * (which orders every layer's work of the call).  Each chunk advances every
- * layer's cascade by its length. */
+ * layer's cascade by its length.  Errors: INVALID_ARG (null pointers), SHAPE
+ * (T < 1, m < 1 or m > max_stride) before anything is enqueued; CUDA if a copy
+ * or a GEMM fails, or the status of a failing cascade_prefill_stride (whose own
+ * rules apply: after a state-mutating failure the handle is POISONED) -- chunks
+ * before the failing one stay enqueued. */
 cascade_status cascade_stack_prefill(cascade_stack* s, const void* x, int64_t T, int32_t m, void* y,
                                      void* stream);
 
