@@ -30,9 +30,6 @@
 #ifndef CASCADE_FWD_EMU
 #define CASCADE_FWD_EMU 4
 #endif
-#ifndef CASCADE_FWD_KS
-#define CASCADE_FWD_KS 0
-#endif
 #ifndef CASCADE_SCORE_EMU
 #define CASCADE_SCORE_EMU 4
 #endif
@@ -66,127 +63,6 @@ __device__ unsigned long long* g_p2_trace = nullptr;
 #define P2_ACC(v)
 #endif
 
-// Pass 1 key-split softmax (KS): two softmax warps per SM sub-partition.  Warps 4-7 own keys
-// [0, 64) of every tile row, warps 8-11 keys [64, 128) (warp w and w + 4 share sub-partition w % 4
-// and TMEM lanes 32 (w % 4)), so one warp's TMEM loads and dependency stalls hide under the
-// other's exp2.  The halves never meet per tile: both exponentiate against the row's reference
-// m_ref = max of tile 0 (exchanged once through shared memory) instead of a running max, so P
-// may exceed 1 by any factor up to 2^kOvf (fp32 / bf16 keep their relative precision; O and l stay
-// far from overflow); a tile sum at or above 2^kOvf (or inf / NaN) flags the row and the CTA
-// re-runs the row with the reference raised (see the epilogue).  Each half writes its P into the
-// first 32 columns of its OWN S region (never a column the other half still has to read).
-template <int D, int EMU>
-__device__ __forceinline__ void attn_fwd_ks_softmax(const TcParams& p, uint32_t tmem, int warp, int lane, int q0,
-                                                    int b, int h, int nt, uint64_t* s_full, uint64_t* p_full,
-                                                    uint64_t* q_full, uint64_t* const* pv_done, float* sRed) {
-  constexpr uint32_t kColO = 256, kColQ = 384;
-  const int half = (warp - 4) >> 2;
-  const int r = (threadIdx.x - 128) & 127;                // query row = TMEM lane
-  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  const int qi = q0 + r;
-  if (half == 0) {   // Q row -> TMEM (A operand of every QK^T)
-    const uint4* src = reinterpret_cast<const uint4*>(p.q_rot + (((long long)b * p.Hq + h) * p.M + qi) * D);
-    const bool in_buf = qi < p.M;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t w[16];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint4 u = in_buf ? src[c * 4 + v] : make_uint4(0u, 0u, 0u, 0u);
-        w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
-      }
-      tc::tmem_st16(tmem + kColQ + lane_off + c * 16, w);
-    }
-    tc::tmem_wait_st();
-    tc::tc_fence_before();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(q_full);
-  }
-  const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-  float l = 0.f, m_ref = 0.f;
-  float x[64];
-  for (int j = 0; j < nt; ++j) {
-    const uint32_t sb = tmem + (j & 1) * 128 + half * 64 + lane_off;
-    tc::mbar_wait_unbounded(s_full + (j & 1), (j >> 1) & 1);
-    tc::tc_fence_after();
-    tc::tmem_ld32(sb, x);
-    tc::tmem_ld32(sb + 32, x + 32);
-    tc::tmem_wait_ld();
-    int lim;                                              // keys [0, lim) of the tile are visible
-    if (j < p.n_res_tiles) {
-      lim = p.res_tiles[j].y;
-    } else {
-      const int k0 = (j - p.n_res_tiles) * 128;
-      lim = min(qi - k0 + 1, p.m - k0);
-    }
-    if (lim < 128) {
-      const int lh = lim - half * 64;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) x[c] = c < lh ? x[c] : -INFINITY;
-    }
-    if (j == 0) {                                         // the reference: the max of tile 0
-      float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 64; c += 4) {
-        m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
-      }
-      sRed[half * 128 + r] = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-      tc::named_bar_sync_roles(2, 256);
-      const float mx = fmaxf(sRed[r], sRed[128 + r]) * p.scale_log2;
-      m_ref = mx == -INFINITY ? 0.f : mx;
-    }
-    const float2 nm2 = make_float2(-m_ref, -m_ref);
-    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float2 t = __ffma2_rn(make_float2(x[c * 32 + 2 * e], x[c * 32 + 2 * e + 1]), sc2, nm2);
-        const bool emu = ((e * EMU) % 16) + EMU >= 16;
-        const float2 pp = emu ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
-        if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
-        pk[e] = tc::pack_bf16(pp.x, pp.y);
-      }
-      tc::tmem_st16(sb + c * 16, pk);
-    }
-    const float2 s01 = __fadd2_rn(s0, s1);
-    l += s01.x + s01.y;
-    tc::tmem_wait_st();
-    tc::tc_fence_before();
-    if (j >= 1) tc::mbar_wait_unbounded(pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);   // observe PV(j-1)
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(p_full + (j & 1));
-  }
-  tc::mbar_wait_unbounded(pv_done[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
-  tc::tc_fence_after();
-  // row sum of both halves; the barrier also orders tile 0's max reads before these writes
-  tc::named_bar_sync_roles(2, 256);
-  sRed[half * 128 + r] = l;
-  tc::named_bar_sync_roles(2, 256);
-  const float lt = sRed[r] + sRed[128 + r];
-  const float inv = 1.f / lt;
-  const bool store = qi < p.m;
-  __nv_bfloat16* orow = p.out + (((long long)b * p.m + qi) * p.Hq + h) * D;
-#pragma unroll
-  for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {   // each half stores D / 2 columns
-    float o[32];
-    tc::tmem_ld32(tmem + kColO + lane_off + c * 32, o);
-    tc::tmem_wait_ld();
-    if (store) {
-      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-        dst[v] = make_uint4(tc::pack_bf16(o[8 * v + 0] * inv, o[8 * v + 1] * inv),
-                            tc::pack_bf16(o[8 * v + 2] * inv, o[8 * v + 3] * inv),
-                            tc::pack_bf16(o[8 * v + 4] * inv, o[8 * v + 5] * inv),
-                            tc::pack_bf16(o[8 * v + 6] * inv, o[8 * v + 7] * inv));
-    }
-  }
-  if (half == 0)
-    p.qbias[((long long)b * p.Hq + h) * p.Mb + qi] = store ? m_ref + log2f(lt) - p.log2w[qi] : INFINITY;
-}
-
 // Pass 1.  Shared-memory bandwidth (128 B/clk/SM) is the binding resource of a 128x128 MMA
 // with both operands in SMEM, so Q and P live in TMEM (A operand from TMEM, "TS" MMAs) and
 // only K/V stream through SMEM (3-stage TMA ring).  TMEM columns: S0 [0,128), S1 [128,256),
@@ -203,8 +79,8 @@ __device__ __forceinline__ void attn_fwd_ks_softmax(const TcParams& p, uint32_t 
 // TMEM accumulator (double-buffered); the softmax warps read tile j-1's column sums while tile j's
 // MMAs run and atomically add them to s_heads.  K/V use a 2-stage ring to make room for the two
 // P buffers (64 KB).
-template <int D, int EMU, bool EST, bool KS>
-__global__ void __launch_bounds__(KS ? 384 : 256, 1)
+template <int D, int EMU, bool EST>
+__global__ void __launch_bounds__(256, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_vs, const __grid_constant__ CUtensorMap tm_vc,
                    TcParams p) {
@@ -226,8 +102,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
   uint64_t* pv_done[2] = {bars + 11, bars + 14};   // PV of tiles j with j % 2 == i
   uint64_t* cs_done = bars + 12;     // [2] EST: column sums of tile j in TMEM buffer j % 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  float* sRed = reinterpret_cast<float*>(bars + 16);    // KS: [2 halves][128 rows] max / sum exchange
-  static_assert(!(KS && EST), "the key-split softmax has no one-pass estimator");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -239,7 +113,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) { tc::mbar_init(kv_full + i, 1); tc::mbar_init(kv_empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, KS ? 8 : 4); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(s_full + i, 1); tc::mbar_init(p_full + i, 4); }
     tc::mbar_init(q_full, 4);
     tc::mbar_init(pv_done[0], 1);
     tc::mbar_init(pv_done[1], 1);
@@ -279,9 +153,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
           vrow = (int)(bg * p.M + k0);
           vm = &tm_vc;
         }
-#ifdef CASCADE_T_HALFKV
-        if (j & 1) { tc::mbar_arrive(kv_full + s); continue; }   // timing experiment only: stale K/V
-#endif
         tc::mbar_expect_tx(kv_full + s, 2 * KB * kTileBytes);
         uint8_t* k_dst = sK + s * KB * kTileBytes;
         uint8_t* v_dst = sV + s * KB * kTileBytes;
@@ -325,13 +196,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         }
         tc::tc_fence_after();
         const uint32_t vbase = aV + (j % kStages) * KB * kTileBytes;
-        // P of keys [0, 64) and [64, 128): both halves of S's upper 64 columns, or (KS) the first 32
-        // columns of each half's own S region
-        const uint32_t pb0 = tmem + (j & 1) * 128 + (KS ? 0 : 64), pb1 = pb0 + (KS ? 64 : 32);
+        const uint32_t pbase = tmem + (j & 1) * 128 + 64;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {             // 128 keys = 8 x K16
           const uint64_t db = tc::desc_mnmajor_sw128(vbase + kk * 2048, kTileBytes);
-          tc::mma_bf16_ts(tmem + kColO, (kk < 4 ? pb0 : pb1) + (kk & 3) * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_bf16_ts(tmem + kColO, pbase + kk * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         if (j + kStages < nt) tc::mma_commit(kv_empty + (j % kStages));   // the producer waits only these
         tc::mma_commit(pv_done[j & 1]);
@@ -366,8 +235,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
       }
 #endif
     }
-  } else if (KS && warp >= 4) {
-    attn_fwd_ks_softmax<D, EMU>(p, tmem, warp, lane, q0, b, h, nt, s_full, p_full, q_full, pv_done, sRed);
   } else if (warp >= 4) {
     // ---------------- softmax warpgroup ----------------
     const int r = threadIdx.x - 128;                      // query row = TMEM lane
@@ -454,11 +321,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             // EMU of every 16 pairs on the FMA pipe (degree-3 polynomial; P is rounded to bf16
             // anyway), the rest on MUFU
             const bool emu = ((e * EMU) % 16) + EMU >= 16;
-#ifdef CASCADE_T_P1_NOEXP
-            const float2 pp = t;                          // timing experiment only: no exp2
-#else
             const float2 pp = emu ? tc::exp2_poly2<3>(t) : make_float2(tc::fast_exp2(t.x), tc::fast_exp2(t.y));
-#endif
             if (e & 1) s1 = __fadd2_rn(s1, pp); else s0 = __fadd2_rn(s0, pp);
             pk[e] = tc::pack_bf16(pp.x, pp.y);
           }
@@ -497,11 +360,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         // hold every PV up to tile j-1 first.
         const float sum = exp_pass(m_used == -INFINITY ? 0.f : m_used, mraw, Track{});
         const float mx = mraw * p.scale_log2;
-#ifdef CASCADE_T_P1_NOEXP
-        const bool need = false;
-#else
         const bool need = mx > m_used + 8.f;
-#endif
         if (__any_sync(0xffffffffu, need)) {
           {
             P1_T0();
@@ -607,12 +466,8 @@ __device__ __forceinline__ void score_chunk(const float* x, const float* bq, flo
     // EMU of every 16 exp2 pairs on the FMA pipe (degree-DEG polynomial), the rest on MUFU
     const int q0i = (e >> 1), q1i = (e >> 1) + 1;           // pair indices 0..15 of this chunk
     const bool e0 = ((q0i * EMU) % 16) + EMU >= 16, e1 = ((q1i * EMU) % 16) + EMU >= 16;
-#ifdef CASCADE_T_NOMUFU
-    float2 p0 = t0, p1 = t1;                              // timing experiment only: no exp2
-#else
     float2 p0 = e0 ? tc::exp2_poly2<DEG>(t0) : make_float2(tc::fast_exp2(t0.x), tc::fast_exp2(t0.y));
     float2 p1 = e1 ? tc::exp2_poly2<DEG>(t1) : make_float2(tc::fast_exp2(t1.x), tc::fast_exp2(t1.y));
-#endif
     if (CUT) {
       p0.x = e + 0 >= cut_from ? p0.x : 0.f;
       p0.y = e + 1 >= cut_from ? p0.y : 0.f;
@@ -741,9 +596,6 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
           const uint32_t kbase = aK + w * KB * kTileBytes;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-#ifdef CASCADE_T_HALFMMA
-            if (kk & 1) continue;                        // timing experiment only: wrong results
-#endif
             const uint64_t da = tc::desc_kmajor_sw128(kbase + (kk >> 2) * kTileBytes + (kk & 3) * 32);
             const uint64_t db = tc::desc_kmajor_sw128(qb + (kk >> 2) * kTileBytes + (kk & 3) * 32);
             tc::mma_bf16_ss(tmem + (2 * sb2 + w) * 128, da, db, idesc, kk > 0 ? 1u : 0u);
@@ -877,7 +729,7 @@ attn_score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 size_t attn_fwd_tc_smem(int d, bool est) {
   const int KB = d / 64;
   return est ? 1024 + (size_t)(2 * 2 * KB) * kTileBytes + 2 * 2 * kTileBytes + 2 * 4096 + 16 * 8 + 64
-             : 1024 + (size_t)(2 * 3 * KB) * kTileBytes + 16 * 8 + 2 * 128 * 4 + 64;
+             : 1024 + (size_t)(2 * 3 * KB) * kTileBytes + 16 * 8 + 64;
 }
 size_t attn_score_tc_smem(int d, int G) {
   const int KB = d / 64;
@@ -892,9 +744,9 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
   const size_t smem = attn_fwd_tc_smem(d, est);
   // 4 of every 16 exp2 pairs on the FMA pipe: measured 75.1 / 78.3 / 78.4 / 76.0 % of peak for
   // 0 / 4 / 6 / 8 (scripts/kbench.py, steady state n_c = 62.5K)
-  auto go = [&](auto kern, int threads) {
+  auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, threads, smem, st>>>(tq, tk, tvs, tvc, p);
+    kern<<<grid, 256, smem, st>>>(tq, tk, tvs, tvc, p);
   };
 #ifdef CASCADE_PASS1_TRACE
   static unsigned long long* trace = nullptr;
@@ -906,12 +758,11 @@ void launch_attn_fwd_tc(const TcParams& p, const CUtensorMap& tq, const CUtensor
   }
 #endif
   if (est) {
-    if (d == 128) go(attn_fwd_tc_kernel<128, 4, true, false>, 256);
-    else go(attn_fwd_tc_kernel<64, 4, true, false>, 256);
+    if (d == 128) go(attn_fwd_tc_kernel<128, 4, true>);
+    else go(attn_fwd_tc_kernel<64, 4, true>);
   } else {
-    constexpr bool ks = CASCADE_FWD_KS != 0;
-    if (d == 128) go(attn_fwd_tc_kernel<128, CASCADE_FWD_EMU, false, ks>, ks ? 384 : 256);
-    else go(attn_fwd_tc_kernel<64, 4, false, ks>, ks ? 384 : 256);
+    if (d == 128) go(attn_fwd_tc_kernel<128, CASCADE_FWD_EMU, false>);
+    else go(attn_fwd_tc_kernel<64, 4, false>);
   }
 #ifdef CASCADE_PASS1_TRACE
   if (++calls % 16 == 0 && ctas <= 4096LL * 64) {
