@@ -101,7 +101,7 @@ Sizes compute_sizes(const cascade_config& c) {
   // sel (3M) + sel_order (M) + mov (2 (N+1) M) + w (M floats) + log2w (M floats)
   // + resident key tiles (2 ints each, <= S/128 + N + 2 of them)
   z.plan_ints = (int32_t)(3 * M + M + 2 * (N + 1) * M + 2 * M + 6 * (S / 128 + 2 * N + 2) + (N + 3) +
-                          2 * 4 * 2 * (N + 1) * M + 48);   // + maintenance moves and their units (4 ints each, <= 2 (N+1) M)
+                          4 * 2 * (N + 1) * M + 48);   // + maintenance moves (4 ints each, <= 2 (N+1) M)
   z.plan = align_up((size_t)z.plan_ints * 4);
   z.resolved = align_up(B * Hk * M * 4);
   z.q_rot = align_up(B * Hq * M * d * es);
@@ -141,9 +141,6 @@ struct Upload {
   int32_t n_maint_staged;
   const int4* maint_chunk;     // moves that read no resident slot (MaintItems::chunk)
   int32_t n_maint_chunk;
-  const int4* maint_units;     // component units {staged begin, count, chunk begin, count}, or null
-  int32_t n_maint_units;       //   (0: the cooperative grid-barrier launch)
-  int32_t maint_unit_rows;     // most staged rows of one unit
 };
 
 // An attend (cascade_attend) whose commit is outstanding, per layer.  The host Plan is shared by
@@ -201,8 +198,6 @@ struct cascade_handle {
   // maintenance planning scratch
   std::vector<int32_t> maint_reads;
   std::vector<int4> maint_staged, maint_chunk;
-  std::vector<int32_t> maint_writer, maint_parent, maint_comp;   // component partition scratch
-  std::vector<int4> maint_units, maint_staged_u, maint_chunk_u;
 };
 
 namespace {
@@ -546,85 +541,14 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   std::vector<int4>& chunk_moves = h->maint_chunk;
   staged.clear();
   chunk_moves.clear();
-  // Component partition: a move that reads a pre-chunk slot is joined (union-find) with the move
-  // that overwrites that slot, so no slot read by one component is written by another.  Each
-  // component can then load all its sources and store all its rows inside one block, with no
-  // grid-wide barrier (maint_comp_kernel).  In the steady state a component is one aligned run
-  // of 2^(N-1) stream indices (a token selected against at sub-cache i interacts with the last
-  // 2^(i-1) tokens only).
-  const size_t E = P.mov.size() / 2;
-  std::vector<int32_t>& wr = h->maint_writer;
-  std::vector<int32_t>& par = h->maint_parent;
-  std::vector<int32_t>& comp = h->maint_comp;
-  if (wr.size() != (size_t)S_tot) wr.assign(S_tot, -1);
-  par.resize(E);
-  for (size_t e = 0; e < E; ++e) { par[e] = (int32_t)e; wr[P.mov[2 * e]] = (int32_t)e; }
-  auto find = [&](int32_t x) {
-    while (par[x] != x) { par[x] = par[par[x]]; x = par[x]; }
-    return x;
-  };
-  std::vector<uint8_t> is_staged(E);
-  for (size_t e = 0; e < E; ++e) {
+  for (size_t e = 0; e < P.mov.size() / 2; ++e) {
     const int32_t dst = P.mov[2 * e], ref = P.mov[2 * e + 1];
     int32_t cand = 0, inc = 0;
     if (ref < 0) { cand = P.sel[3 * (-ref - 1) + 1]; inc = P.sel[3 * (-ref - 1) + 2]; }
     rd.clear();
     reads(ref, reads);
-    is_staged[e] = !rd.empty();
     (rd.empty() ? chunk_moves : staged).push_back(make_int4(dst, ref, cand, inc));
-    for (int32_t x : rd) {
-      const int32_t w = wr[x];
-      if (w >= 0) { const int32_t a = find((int32_t)e), b = find(w); if (a != b) par[a] = b; }
-    }
   }
-  for (size_t e = 0; e < E; ++e) wr[P.mov[2 * e]] = -1;
-  // components in order of first appearance, packed into units of <= kUnitRows staged rows
-  const int32_t kUnitMaxRows = maint_unit_cap(h->cfg.head_dim, (int)elem_size(h->cfg.dtype));
-  const int32_t kUnitRows = std::min<int32_t>(192, kUnitMaxRows), kUnitChunk = 384;
-  std::vector<int4>& units = h->maint_units;
-  std::vector<int4>& st_u = h->maint_staged_u;
-  std::vector<int4>& ch_u = h->maint_chunk_u;
-  units.clear(); st_u.clear(); ch_u.clear();
-  int32_t unit_rows = 0;
-  {
-    comp.assign(E, -1);                                  // root -> component index
-    std::vector<int32_t> cst, cch;                       // per component: staged / chunk counts
-    std::vector<int32_t> cof(E);
-    int32_t ncomp = 0;
-    for (size_t e = 0; e < E; ++e) {
-      const int32_t r = find((int32_t)e);
-      if (comp[r] < 0) { comp[r] = ncomp++; cst.push_back(0); cch.push_back(0); }
-      cof[e] = comp[r];
-      (is_staged[e] ? cst : cch)[comp[r]]++;
-    }
-    bool ok = true;
-    for (int32_t c = 0; c < ncomp && ok; ++c) ok = cst[c] <= kUnitMaxRows;
-    if (ok && E > 0) {
-      // unit of each component, then the moves bucketed by unit (counting sort)
-      std::vector<int32_t> cu(ncomp);
-      int32_t nu = 0, us = 0, uc = 0;
-      for (int32_t c = 0; c < ncomp; ++c) {
-        if (nu == 0 || us + cst[c] > kUnitRows || (cst[c] == 0 && uc + cch[c] > kUnitChunk)) {
-          units.push_back(make_int4(0, 0, 0, 0));
-          ++nu; us = 0; uc = 0;
-        }
-        cu[c] = nu - 1; us += cst[c]; uc += cch[c];
-        units[nu - 1].y += cst[c]; units[nu - 1].w += cch[c];
-      }
-      int32_t so = 0, co = 0;
-      for (auto& u : units) { u.x = so; u.z = co; so += u.y; co += u.w; unit_rows = std::max(unit_rows, u.y); }
-      st_u.resize(so); ch_u.resize(co);
-      std::vector<int32_t> fs(nu), fc(nu);
-      for (int32_t u = 0; u < nu; ++u) { fs[u] = units[u].x; fc[u] = units[u].z; }
-      size_t si = 0, ci = 0;
-      for (size_t e = 0; e < E; ++e) {
-        const int32_t u = cu[cof[e]];
-        if (is_staged[e]) st_u[fs[u]++] = staged[si++];
-        else ch_u[fc[u]++] = chunk_moves[ci++];
-      }
-    }
-  }
-  const bool use_units = !units.empty();
   // layout of the upload (int32 words): sel | sel_order | mov | w [m] | log2w [m] | tiles (int2) |
   // phase_begin | dec tiles (int4) | staged moves (int4) | chunk moves (int4); every capacity is
   // checked before anything is written into the pinned buffer
@@ -635,8 +559,7 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   const size_t dt_off = pad4(ph_off + P.phase_begin.size());
   const size_t mi_off = pad4(dt_off + 4 * dt.size());
   const size_t cm_off = mi_off + 4 * staged.size();
-  const size_t un_off = cm_off + 4 * chunk_moves.size();
-  const size_t total = un_off + 4 * units.size();
+  const size_t total = cm_off + 4 * chunk_moves.size();
   if (total > (size_t)h->sz.plan_ints) return CASCADE_ERR_WORKSPACE;   // capacity formula broken
   const int slot = h->ring_pos;
   if (cudaEventSynchronize(h->ring_ev[slot]) != cudaSuccess) return CASCADE_ERR_CUDA;
@@ -656,10 +579,8 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   std::memcpy(buf + tiles_off, tiles.data(), tiles.size() * sizeof(int2));
   std::memcpy(buf + ph_off, P.phase_begin.data(), P.phase_begin.size() * 4);
   std::memcpy(buf + dt_off, dt.data(), dt.size() * sizeof(int4));
-  // unit order when the component launch runs, else phase order (the cooperative launch's rounds)
-  std::memcpy(buf + mi_off, (use_units ? st_u : staged).data(), staged.size() * sizeof(int4));
-  std::memcpy(buf + cm_off, (use_units ? ch_u : chunk_moves).data(), chunk_moves.size() * sizeof(int4));
-  std::memcpy(buf + un_off, units.data(), units.size() * sizeof(int4));
+  std::memcpy(buf + mi_off, staged.data(), staged.size() * sizeof(int4));
+  std::memcpy(buf + cm_off, chunk_moves.data(), chunk_moves.size() * sizeof(int4));
   LayerBufs& L = h->layers[layer];
   if (cudaMemcpyAsync(L.plan, buf, total * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return CASCADE_ERR_CUDA;
@@ -680,9 +601,6 @@ cascade_status upload_plan(cascade_handle* h, int32_t layer, int32_t m, cudaStre
   up->n_maint_staged = (int32_t)staged.size();
   up->maint_chunk = reinterpret_cast<const int4*>(L.plan + cm_off);
   up->n_maint_chunk = (int32_t)chunk_moves.size();
-  up->maint_units = use_units ? reinterpret_cast<const int4*>(L.plan + un_off) : nullptr;
-  up->n_maint_units = (int32_t)units.size();
-  up->maint_unit_rows = unit_rows;
   return CASCADE_OK;
 }
 
@@ -749,9 +667,6 @@ bool launch_maintenance(cascade_handle* h, const Geometry& g, LayerBufs& L, cons
   it.n_staged = up.n_maint_staged;
   it.chunk = up.maint_chunk;
   it.n_chunk = up.n_maint_chunk;
-  it.units = up.maint_units;
-  it.n_units = up.n_maint_units;
-  it.unit_rows = up.maint_unit_rows;
   it.barrier = L.maint_ctl;
   it.barrier_base = L.maint_barrier;
   StateDev<T> sd{reinterpret_cast<T*>(L.k_raw), reinterpret_cast<T*>(L.v), L.mu, L.origin, k, v};

@@ -1,8 +1,6 @@
 // internal.h -- shared between the host control plane and the kernels (library-private).
 #pragma once
 
-#include <algorithm>
-
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -99,14 +97,8 @@ struct MaintItems {
   int32_t rows_per_block;     // set by launch_maint
   unsigned long long* moved;  // [B*Hkv] rows rewritten by staged moves (selection outcomes)
   int32_t inline_sel;         // 1: every selection is depth 0, resolved where its winner moves
-  const int4* units;          // component units {staged begin, n, chunk begin, n} (staged / chunk in
-  int32_t n_units;            //   unit order), or null: the cooperative grid-barrier launch
-  int32_t unit_rows;          // most staged rows of one unit (<= 256)
 };
 struct MaintGrid { int blocks, rows_per_block; };
-// most staged rows of one maint_comp_kernel unit: one thread per row (256) and the rows' K, V, mu,
-// origin and destination (2 d es + 24 bytes each) within 220 KB of shared memory
-inline int maint_unit_cap(int d, int es) { return std::min(256, (int)(220 * 1024 / (2 * d * es + 24))); }
 template <typename T>
 cudaError_t launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
                   cudaStream_t st);

@@ -31,12 +31,6 @@
 #include <cstdlib>
 #include <vector>
 
-// 1: a chunk whose moves split into components of <= 256 staged rows runs maint_comp_kernel
-// (no grid barrier); 0: always the cooperative launch
-#ifndef CASCADE_MAINT_COMP
-#define CASCADE_MAINT_COMP 0
-#endif
-
 namespace cascade {
 
 __device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
@@ -392,162 +386,6 @@ __global__ void __launch_bounds__(kCoopThreads, 2) maint_coop_kernel(Geometry g,
   if (threadIdx.x == 0 && s_moved) atomicAdd(it.moved + blockIdx.x % BG, (unsigned long long)s_moved);
 }
 
-
-// maint_comp_kernel: one block per (component unit, b*g), no grid barrier.  The host grouped the
-// chunk's moves so that every pre-chunk slot a unit reads is written, if at all, by a move of the
-// same unit (cascade_host.cu, component partition); a block therefore loads all its staged rows
-// (selections resolved in place, strict '>'), waits for them, then stores them and streams
-// its chunk-row moves -- blocks never wait for each other, so one block's stores overlap another's
-// loads across the GPU.
-constexpr int kCompThreads = 256;
-constexpr int kCU = 8;                                     // chunk rows per warp in flight
-template <typename T, int VPL>
-__global__ void __launch_bounds__(kCompThreads) maint_comp_kernel(Geometry g, PlanDev p, MaintItems it,
-                                                                  StateDev<T> sd, const float* __restrict__ s) {
-  extern __shared__ __align__(16) int4 s_rows[];          // [it.unit_rows][2 * nvec]
-  const int R = it.unit_rows;
-  const int nvec = g.d * (int)sizeof(T) / 16;
-  double* s_mu = reinterpret_cast<double*>(s_rows + (size_t)R * 2 * nvec);
-  int64_t* s_org = reinterpret_cast<int64_t*>(s_mu + R);
-  long long* s_doff = reinterpret_cast<long long*>(s_org + R);
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_moved;
-  const int4 un = it.units[blockIdx.x];
-  const int bg = blockIdx.y;
-  auto mark = [&](int k) {
-    if (g_maint_trace && threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      g_maint_trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + k] = t;
-    }
-  };
-  mark(0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t row_bytes = (uint32_t)(g.d * sizeof(T));
-  const long long sb = (long long)bg * g.S_tot;
-  const double* mu = sd.mu + sb;
-  const float* sbg = s + (long long)bg * (g.S_tot + g.m);
-  if (threadIdx.x == 0) {
-    s_moved = 0;
-    tc::mbar_init(&s_bar, kCompThreads);
-    tc::fence_mbar_init();
-  }
-  __syncthreads();
-  // loads: thread j < n stages move j's source row (K, V by bulk copy; mu, origin by the thread)
-  const int j = threadIdx.x;
-  uint32_t moved = 0;
-  {
-    bool issued = false;
-    if (j < un.y) {
-      const int4 mv = it.staged[un.x + j];               // dst, ref, cand, inc
-      int32_t src = mv.y;
-      if (src < 0)
-        src = it.inline_sel ? (src_mu(g, mv.z, mu, sbg) > src_mu(g, mv.w, mu, sbg) ? mv.z : mv.w)
-                            : p.resolved[(long long)bg * p.sel_cap + (-src - 1)];
-      const bool mv_row = src != mv.x;                     // resident won its selection: stays
-      moved = mv_row ? 1u : 0u;
-      s_doff[j] = mv_row ? sb + mv.x : -1;
-      if (mv_row) {
-        const T *ks, *vs;
-        if (src < g.S_tot) {
-          ks = sd.k_raw + (sb + src) * g.d;
-          vs = sd.v + (sb + src) * g.d;
-        } else {
-          const int r = src - g.S_tot, gg = bg % g.Hkv, b = bg / g.Hkv;
-          ks = sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-          vs = sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d;
-        }
-        uint8_t* row = reinterpret_cast<uint8_t*>(s_rows + (size_t)j * 2 * nvec);
-        tc::mbar_expect_tx(&s_bar, 2 * row_bytes);
-        tc::bulk_load(row, ks, row_bytes, &s_bar);
-        tc::bulk_load(row + row_bytes, vs, row_bytes, &s_bar);
-        issued = true;
-        s_mu[j] = src_mu(g, src, mu, sbg);                 // folded (Q9) or a new token's s
-        s_org[j] = src < g.S_tot ? sd.origin[sb + src] : g.t0 + (src - g.S_tot);
-      }
-    }
-    if (!issued) tc::mbar_arrive(&s_bar);
-  }
-  // chunk-row moves (sources never overwritten; destinations may be staged sources, so their
-  // stores wait for the unit's loads): kCU rows per warp in flight, the first batch loaded
-  // before the wait
-  {
-    const int gg = bg % g.Hkv, b = bg / g.Hkv;
-    constexpr int kWarps = kCompThreads / 32;
-    int4 buf[kCU][VPL];
-    int32_t dst[kCU], src[kCU];
-    auto batch_load = [&](int c0) {
-#pragma unroll
-      for (int u = 0; u < kCU; ++u) {
-        dst[u] = -1;
-        if (c0 + u >= un.w) continue;
-        const int4 mv = it.chunk[un.z + c0 + u];
-        int32_t sr = mv.y;
-        if (sr < 0)
-          sr = it.inline_sel ? ((double)sbg[mv.z] > (double)sbg[mv.w] ? mv.z : mv.w)   // P:615, strict
-                             : p.resolved[(long long)bg * p.sel_cap + (-sr - 1)];
-        dst[u] = mv.x; src[u] = sr;
-        const int r = sr - g.S_tot;
-        const int4* ks = reinterpret_cast<const int4*>(sd.k_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
-        const int4* vs = reinterpret_cast<const int4*>(sd.v_in + (((long long)b * g.m + r) * g.Hkv + gg) * g.d);
-#pragma unroll
-        for (int hh = 0; hh < VPL; ++hh) {
-          const int i = lane + 32 * hh;
-          if (i < nvec) buf[u][hh] = __ldcs(ks + i);
-          else if (i < 2 * nvec) buf[u][hh] = __ldcs(vs + i - nvec);
-        }
-      }
-    };
-    auto batch_store = [&]() {
-#pragma unroll
-      for (int u = 0; u < kCU; ++u) {
-        if (dst[u] < 0) continue;
-        int4* kd = reinterpret_cast<int4*>(sd.k_raw + (sb + dst[u]) * g.d);
-        int4* vd = reinterpret_cast<int4*>(sd.v + (sb + dst[u]) * g.d);
-#pragma unroll
-        for (int hh = 0; hh < VPL; ++hh) {
-          const int i = lane + 32 * hh;
-          if (i < nvec) __stcs(kd + i, buf[u][hh]);
-          else if (i < 2 * nvec) __stcs(vd + i - nvec, buf[u][hh]);
-        }
-        if (lane == 0) {
-          sd.mu[sb + dst[u]] = (double)sbg[src[u]];                 // mu = s
-          sd.origin[sb + dst[u]] = g.t0 + (src[u] - g.S_tot);
-        }
-      }
-    };
-    batch_load(warp * kCU);                                 // first batch: in flight with the staged loads
-    mark(1);
-    tc::mbar_wait(&s_bar, 0);                                // every source of the unit is read
-    mark(2);
-    tc::fence_proxy_async_smem();
-    if (j < un.y && s_doff[j] >= 0) {
-      const long long doff = s_doff[j];
-      const uint8_t* row = reinterpret_cast<const uint8_t*>(s_rows + (size_t)j * 2 * nvec);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sd.k_raw + doff * g.d),
-                   "r"(tc::smem_u32(row)), "r"(row_bytes)
-                   : "memory");
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sd.v + doff * g.d),
-                   "r"(tc::smem_u32(row + row_bytes)), "r"(row_bytes)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      sd.mu[doff] = s_mu[j];
-      sd.origin[doff] = s_org[j];
-    }
-    mark(3);
-    for (int c0 = warp * kCU; c0 < un.w; c0 += kWarps * kCU) {
-      if (c0 != warp * kCU) batch_load(c0);
-      batch_store();
-    }
-    mark(4);
-  }
-  if (moved) atomicAdd(&s_moved, moved);
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem rows read before exit
-  __syncthreads();
-  if (threadIdx.x == 0 && s_moved) atomicAdd(it.moved + bg, (unsigned long long)s_moved);
-  mark(5);
-}
-
 template <typename T>
 size_t maint_coop_smem(int d, int rows) {
   return (size_t)rows * 2 * d * sizeof(T) + (size_t)rows * (8 + 8 + 8) + 16;
@@ -579,51 +417,22 @@ template <typename T>
 cudaError_t launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, StateDev<T> sd, const float* s,
                          cudaStream_t st) {
   if (it.n_staged <= 0 && it.n_chunk <= 0) return cudaSuccess;
-  static unsigned long long* trace = nullptr;
-  static int trace_on = -1, trace_n = 0;
-  if (trace_on < 0) {
-    const char* e = std::getenv("CASCADE_MAINT_TRACE");
-    trace_on = e && std::atoi(e) > 0 ? std::atoi(e) : 0;
-    if (trace_on) {
-      cudaMalloc(&trace, (size_t)65536 * 8 * 8);
-      cudaMemcpyToSymbol(g_maint_trace, &trace, sizeof(trace));
-    }
-  }
-  if (it.units && it.n_units > 0 && CASCADE_MAINT_COMP) {   // component units: no grid barrier
-    const int vpl = 2 * g.d * (int)sizeof(T) / 16 > 32 ? 2 : 1;
-    auto kern = vpl == 2 ? maint_comp_kernel<T, 2> : maint_comp_kernel<T, 1>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[vpl - 1]) {
-      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)maint_coop_smem<T>(g.d, maint_unit_cap(g.d, (int)sizeof(T))));
-      if (e != cudaSuccess) return e;
-      attr_set[vpl - 1] = true;
-    }
-    const size_t smem = maint_coop_smem<T>(g.d, std::max(it.unit_rows, 1));
-    kern<<<dim3(it.n_units, g.B * g.Hkv), kCompThreads, smem, st>>>(g, p, it, sd, s);
-    if (trace_on && ++trace_n == trace_on) {   // dump the n-th launch: per-block marks, ns
-      const int nb = it.n_units * g.B * g.Hkv;
-      std::vector<unsigned long long> h((size_t)nb * 8);
-      cudaStreamSynchronize(st);
-      cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
-      unsigned long long t0 = ~0ull, t1 = 0;
-      for (int b = 0; b < nb; ++b) { t0 = std::min(t0, h[b * 8]); t1 = std::max(t1, h[b * 8 + 5]); }
-      std::fprintf(stderr, "maint comp trace: %d units x %d, unit rows %d, staged %d chunk %d, span %.2f us\n"
-                   "block start issued waited staged_stored chunks_done end (us)\n",
-                   it.n_units, g.B * g.Hkv, it.unit_rows, it.n_staged, it.n_chunk, (t1 - t0) / 1e3);
-      for (int b = 0; b < nb; b += 1)
-        std::fprintf(stderr, "%d %.2f %.2f %.2f %.2f %.2f %.2f\n", b, (h[b * 8] - t0) / 1e3, (h[b * 8 + 1] - t0) / 1e3,
-                     (h[b * 8 + 2] - t0) / 1e3, (h[b * 8 + 3] - t0) / 1e3, (h[b * 8 + 4] - t0) / 1e3,
-                     (h[b * 8 + 5] - t0) / 1e3);
-    }
-    return cudaGetLastError();
-  }
   const MaintGrid mg = maint_coop_grid<T>(g.d);
   it.rows_per_block = mg.rows_per_block;
   const size_t smem = maint_coop_smem<T>(g.d, mg.rows_per_block);
   void* args[] = {(void*)&g, (void*)&p, (void*)&it, (void*)&sd, (void*)&s};
   const void* kern = 2 * g.d * sizeof(T) / 16 > 32 ? (const void*)maint_coop_kernel<T, 2>
                                                    : (const void*)maint_coop_kernel<T, 1>;
+  static unsigned long long* trace = nullptr;
+  static int trace_on = -1, trace_n = 0;
+  if (trace_on < 0) {
+    const char* e = std::getenv("CASCADE_MAINT_TRACE");
+    trace_on = e && std::atoi(e) > 0 ? std::atoi(e) : 0;
+    if (trace_on) {
+      cudaMalloc(&trace, (size_t)mg.blocks * 8 * 8);
+      cudaMemcpyToSymbol(g_maint_trace, &trace, sizeof(trace));
+    }
+  }
   const cudaError_t rc = cudaLaunchCooperativeKernel(kern, dim3(mg.blocks), dim3(kCoopThreads), args, smem, st);
   if (rc != cudaSuccess) return rc;
   if (trace_on && ++trace_n == trace_on) {     // dump the n-th launch: per-block marks, ns
@@ -643,7 +452,6 @@ cudaError_t launch_maint(const Geometry& g, const PlanDev& p, MaintItems it, Sta
 
 template <typename T>
 int maint_barriers(const Geometry& g, const MaintItems& it) {
-  if (it.units && it.n_units > 0 && CASCADE_MAINT_COMP) return 0;
   const MaintGrid mg = maint_coop_grid<T>(g.d);
   const long long total = (long long)it.n_staged * g.B * g.Hkv;
   const long long per_round = (long long)mg.blocks * mg.rows_per_block;
