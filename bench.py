@@ -585,7 +585,11 @@ def main():
                                   "the EMA fold runs in attn_score's epilogue)",
                         "bound": "hbm", "achieved": rm / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": rm / 1e9 / peaks["hbm"],
-                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)"},
+                        "work": "2 (2 d es + 16) bytes per row actually moved (read + write of K, V, mu, origin)",
+                        "note": "each event-timed launch includes ~5 us of launch and event edge (an empty launch of "
+                                "this shape measures 5.2-6.1 us, profiles/launch_edge_r01.txt); the kernel alone: "
+                                "ncu gpu__time_duration 18.6 us for a steady-state launch moving 65536 rows (69.2 MB) "
+                                "= 57 % of HBM (profiles/ncu_traffic_r02.json), DESIGN.md section 4"},
         "step_useful": {"achieved": w1 / args.steps / (ms_step / 1e3) / 1e12, "unit": "TFLOP/s",
                         "note": "useful attention flops per step / whole step time (every kernel, all streams)"},
     }
