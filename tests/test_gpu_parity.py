@@ -114,13 +114,14 @@ def test_score_injection_homogeneous_bit_exact(idx):
     test_score_injection_state_bit_exact(*SMALL[idx], head_policy="homogeneous")
 
 
-def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_advance=0):
+def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_advance=0, gamma=None):
     spec = dict(CONFIGS[name])
     cfg = C.CascadeConfig(num_layers=1, batch=spec["batch"], num_q_heads=spec["num_q_heads"],
                           num_kv_heads=spec["num_kv_heads"], head_dim=spec["head_dim"],
                           sink_size=spec["sink_size"], cache_size=spec["cache_size"],
                           num_cascades=spec["num_cascades"], max_stride=spec["stride"],
-                          dtype=spec["dtype"], rope_theta=spec["rope_theta"])
+                          dtype=spec["dtype"], rope_theta=spec["rope_theta"],
+                          **({} if gamma is None else {"ema_gamma": gamma}))
     k_idx = int(name[3])
     # margin-audit protocol: the seed advances by +7 per rejected audit
     syn = Synth(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, config_seed(k_idx) + 7 * seed_advance,
@@ -150,10 +151,13 @@ def _run_end_to_end(name, n_chunks=None, check_every=1, passkey_at=None, seed_ad
     return worst_o, worst_s, margins
 
 
-def test_cfg1_toy_end_to_end_fp32():
-    worst_o, worst_s, margins = _run_end_to_end("cfg1_toy")
+@pytest.mark.parametrize("gamma", [None, 0.9])
+def test_cfg1_toy_end_to_end_fp32(gamma):
+    """configs[0] at the paper's gamma = 0.9999 and at 0.9 (a fast EMA, so
+    mu is dominated by the last chunks' scores and the selections see different margins)."""
+    worst_o, worst_s, margins = _run_end_to_end("cfg1_toy", gamma=gamma)
     assert margins.size > 0          # selections happened
-    print(f"cfg1: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
+    print(f"cfg1 gamma={gamma}: max|dO|={worst_o:.2e} max rel ds={worst_s:.2e} min margin={margins.min():.3e}")
 
 
 def test_cfg2_first_chunks_end_to_end_bf16():
